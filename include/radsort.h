@@ -1,0 +1,155 @@
+/* radsort.h -- C ABI of radsort, a B200-native MSD radix sort of fixed-size
+ * records (the hot path of RADULS2, arXiv 1703.00687).
+ *
+ * Problem statement (§1): radix sort "works in k phases, each
+ * phase is related to sorting keys according to the current digit ... MSD ...
+ * starts sorting the data according to the most significant digit. This
+ * results in partitioning data into bins that may be further processed
+ * independently in the recursive manner."  PAPER.md:116 §3.1: "MSD radix sort
+ * with 1 B digits".  Records are fixed-size: a key plus an opaque data field
+ * (§4.2 "16 B records (8 B key and 8 B data)"
+ * §3.3 record layouts).
+ *
+ * Record model (reading R1): record i occupies bytes
+ * [i*rec_size, (i+1)*rec_size).  Its key is bytes [0, key_size) read as a
+ * key_size-byte LITTLE-ENDIAN unsigned integer (key_size = 16: low 8-byte
+ * word at +0, high word at +8).  Digit d (d = 0 most significant) is byte
+ * key_size-1-d.  Order: unsigned, i.e. lexicographic on digits 0..key_size-1.
+ * Bytes [key_size, rec_size) are payload and travel with the key.  The sort is
+ * NOT stable: inside an equal-key run any order is a correct result
+ * (reading R2).
+ *
+ * Every function returns a radsort_status; no C++ exception crosses the ABI.
+ * All pointers named dev_* are device pointers on the current CUDA device.
+ */
+#ifndef RADSORT_H_
+#define RADSORT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RADSORT_OK = 0,
+  RADSORT_ERR_INVALID_ARG = 1,     /* NULL pointer with n > 0, overlap, misalignment, size overflow */
+  RADSORT_ERR_UNSUPPORTED = 2,     /* rec_size / key_size combination not built */
+  RADSORT_ERR_NOT_INITIALIZED = 3, /* radsort_init not called for the current device */
+  RADSORT_ERR_CUDA = 4,            /* a CUDA call failed; detail in radsort_error_string */
+  RADSORT_ERR_NCCL = 5,            /* an NCCL call failed (multi-GPU path) */
+  RADSORT_ERR_OOM = 6,             /* workspace allocation failed */
+  RADSORT_ERR_CAPACITY = 7         /* multi-GPU: output shard would exceed `capacity` */
+} radsort_status;
+
+/* Per-call statistics of the last radsort_sort / radsort_sort_multi on the
+ * calling thread's device.  Kernel times are filled only when timing is
+ * enabled (radsort_set_timing(1)); they are CUDA-event times on the sort's
+ * stream, summed over launches of that kernel class. */
+enum {
+  RADSORT_K_SAMPLE = 0, /* strided sample -> first non-constant digit guess           */
+  RADSORT_K_HIST = 1,   /* per-segment digit histogram + key AND/OR (one read)          */
+  RADSORT_K_PLAN = 2,   /* constant-digit skip, bin bases, tile map (per segment)       */
+  RADSORT_K_SCATTER = 3,/* decoupled-look-back scatter pass (one read + one write)      */
+  RADSORT_K_CHILDREN = 4,/* classify child bins; sort tiny ones; copy final ones        */
+  RADSORT_K_LOCAL = 5,  /* CTA-local shared-memory sort of a bin <= C records           */
+  RADSORT_K_MULTI = 6,  /* multi-GPU exchange-side kernels                               */
+  RADSORT_K_COUNT = 7
+};
+
+typedef struct {
+  uint64_t n;                 /* records sorted on this device                          */
+  uint32_t rec_size, key_size;
+  uint32_t levels;            /* MSD levels executed (host loop iterations)             */
+  uint32_t scatter_passes;    /* data-moving segmented scatter launches                 */
+  uint32_t constant_digits_skipped; /* leading digits constant over the whole input     */
+  uint32_t first_digit;       /* d0: first digit the level-0 scatter used               */
+  uint64_t records_scattered; /* sum over scatter launches of records moved             */
+  uint64_t records_hist;      /* sum over histogram launches of records read            */
+  uint64_t records_local;     /* records finished by the CTA-local sorter               */
+  uint64_t records_tiny;      /* records finished by the warp tiny sorter (in CHILDREN) */
+  uint64_t records_copied;    /* records of final bins copied tmp -> records            */
+  uint64_t bins_large, bins_local, bins_tiny, bins_final; /* children per class         */
+  uint64_t nvlink_bytes_sent, nvlink_bytes_recv;          /* multi-GPU exchange         */
+  uint32_t kernel_launches[RADSORT_K_COUNT];
+  float kernel_ms[RADSORT_K_COUNT];
+  uint64_t kernel_bytes[RADSORT_K_COUNT]; /* algorithmic HBM bytes (read + write)      */
+} radsort_stats;
+
+/* Create the per-(process, device) context for `device` (cudaSetDevice is the
+ * caller's business; this only records the device and queries its
+ * attributes).  Idempotent.  Environment overrides (read here):
+ * RADSORT_LOG=1 prints a per-level summary to stderr. */
+radsort_status radsort_init(int device);
+
+/* Sort n records in place in dev_records (§3.1 general scheme:
+ * whole-array pass by the first digit, then bins by further digits, tiny bins
+ * by a comparison sorter).
+ *   dev_records  n*rec_size bytes, 16-byte aligned; output = same buffer,
+ *                permuted so keys are non-decreasing.
+ *   dev_tmp      scratch of >= n*rec_size bytes, 16-byte aligned, must not
+ *                overlap dev_records; contents undefined afterwards.
+ *   rec_size     8, 16 or 32 (built layouts; 24/40/48/56/64 -> UNSUPPORTED).
+ *   key_size     8 or 16, key_size <= rec_size.
+ *   stream       cudaStream_t (NULL = legacy default stream) on which all
+ *                work is ordered.  The call blocks the host once per MSD level
+ *                for a <= 64-byte summary read and returns with the last
+ *                kernels possibly still running on `stream`.
+ * n = 0 or 1 is a no-op returning RADSORT_OK.  Ownership: the caller owns
+ * both buffers; the library owns only its workspace (grown on demand, freed in
+ * radsort_finalize).  n must be < 2^32.  Concurrent calls on one device are
+ * serialised by an internal mutex. */
+radsort_status radsort_sort(void* dev_records, void* dev_tmp, uint64_t n, uint32_t rec_size,
+                            uint32_t key_size, void* stream);
+
+/* End-to-end variant on HOST memory: copies host_records (n*rec_size bytes,
+ * ideally pinned) to the device, sorts it with radsort_sort, and copies the
+ * sorted records back into host_records.  Device buffers come from the
+ * library workspace.  Synchronous: returns after the result is in host memory. */
+radsort_status radsort_sort_host(void* host_records, uint64_t n, uint32_t rec_size,
+                                 uint32_t key_size, void* stream);
+
+/* Multi-GPU collective sort (one process per GPU; every rank of nccl_comm
+ * calls it with the same rec_size/key_size).  Input: dev_records[0..n_local).
+ * Output: dev_records[0..*n_out) holds this rank's key range; concatenating
+ * the ranks' outputs in rank order equals radsort_sort of the concatenated
+ * inputs (up to order inside equal-key runs).  Exact-balance quotas:
+ * *n_out = floor(N/G) + (rank < N mod G), N = sum of n_local.  Both buffers
+ * must hold >= capacity records and capacity >= *n_out, else every rank
+ * returns RADSORT_ERR_CAPACITY.  nccl_comm is an ncclComm_t created from the
+ * same libnccl this library links (torch's ProcessGroupNCCL._comm_ptr()). */
+radsort_status radsort_sort_multi(void* dev_records, void* dev_tmp, uint64_t n_local,
+                                  uint64_t capacity, uint64_t* n_out, uint32_t rec_size,
+                                  uint32_t key_size, void* nccl_comm, void* stream);
+
+/* Splitter planning used by radsort_sort_multi (pure host function, exposed
+ * for testing).  Given the GLOBAL (allreduced) 256-bin histogram `hist` of
+ * the current digit over a bucket range, per-rank quotas and the global rank
+ * q of a boundary already located inside that bucket range, returns the
+ * bucket b containing global position q and the count of records in buckets
+ * < b (before).  Returns RADSORT_ERR_INVALID_ARG if q >= sum(hist). */
+radsort_status radsort_locate_bucket(const uint64_t* hist256, uint64_t q, uint32_t* bucket,
+                                     uint64_t* before);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event timing in radsort_stats. */
+radsort_status radsort_set_timing(int enable);
+
+/* Statistics of the last sort call on this thread's current device. */
+radsort_status radsort_last_stats(radsort_stats* out);
+
+/* Static description of a status plus, for the last failing call on this
+ * thread, a detail string (e.g. the CUDA error). */
+const char* radsort_error_string(radsort_status s);
+
+/* Free every device's workspace and context.  Safe to call repeatedly. */
+void radsort_finalize(void);
+
+/* Library version, e.g. "radsort 0.1 sm_100a". */
+const char* radsort_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RADSORT_H_ */

@@ -12,8 +12,9 @@ passage it follows):
 - ``digit_hist(records, K, d)``   256-bin histogram of digit d
 - ``key_compare(a, b, K)``        -1 / 0 / +1
 - ``compare(got, want, K)``       canonical parity check (-1 = equal)
+- ``rank_bounds(records, K, key)`` (#keys < k, #keys <= k): sampled full-size checks
 
 Pins: tests/test_oracle.py (brute force, numpy/lexsort special cases, SPEC
 worked examples in tests/golden/).  Parity pinned for every function above.
 """
-from .oracle import sort, digit, digit_hist, key_compare, compare, lib_path, build  # noqa: F401
+from .oracle import sort, digit, digit_hist, key_compare, compare, rank_bounds, lib_path, build  # noqa: F401

@@ -38,6 +38,8 @@ def _load():
         L.oracle_digit_hist.restype = ctypes.c_int
         L.oracle_key_compare.argtypes = [vp, vp, u32]
         L.oracle_key_compare.restype = ctypes.c_int
+        L.oracle_rank_bounds.argtypes = [vp, u64, u32, u32, vp, vp, vp]
+        L.oracle_rank_bounds.restype = ctypes.c_int
         L.oracle_compare.argtypes = [vp, vp, u64, u32, u32]
         L.oracle_compare.restype = ctypes.c_int64
         _lib = L
@@ -88,3 +90,15 @@ def compare(got: np.ndarray, want: np.ndarray, K: int) -> int:
     assert g.shape == w.shape
     n, R = g.shape
     return int(_load().oracle_compare(g.ctypes.data, w.ctypes.data, n, R, K))
+
+
+def rank_bounds(records: np.ndarray, K: int, key_record: np.ndarray):
+    """(#keys < k, #keys <= k) over `records` for the key of `key_record`."""
+    a = _as_records(records)
+    n, R = a.shape
+    k = np.ascontiguousarray(key_record, dtype=np.uint8).reshape(-1)
+    lt = ctypes.c_uint64(0)
+    le = ctypes.c_uint64(0)
+    if _load().oracle_rank_bounds(a.ctypes.data, n, R, K, k.ctypes.data, ctypes.byref(lt), ctypes.byref(le)) != 0:
+        raise ValueError("bad K/R")
+    return int(lt.value), int(le.value)

@@ -81,6 +81,24 @@ int oracle_digit_hist(const uint8_t* in, uint64_t n, uint32_t R, uint32_t K, uin
   return 0;
 }
 
+// Rank bounds of one key value in an unsorted array (plain definition of the
+// sorted position): in any correct sort, the record at output position i has
+// a key k with lt(k) <= i < le(k), lt = #{j: key_j < k}, le = #{j: key_j <= k}.
+// Lets full-size results be checked at sampled positions one by one.
+int oracle_rank_bounds(const uint8_t* in, uint64_t n, uint32_t R, uint32_t K, const uint8_t* key_rec,
+                       uint64_t* lt, uint64_t* le) {
+  if (K > R) return -1;
+  uint64_t a = 0, b = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint8_t* r = in + i * R;
+    if (key_less(r, key_rec, K)) ++a;
+    else if (key_equal(r, key_rec, K)) ++b;
+  }
+  *lt = a;
+  *le = a + b;
+  return 0;
+}
+
 // Three-way key comparison of two single records: -1, 0, +1.
 int oracle_key_compare(const uint8_t* a, const uint8_t* b, uint32_t K) {
   if (key_less(a, b, K)) return -1;

@@ -1,0 +1,7 @@
+"""radsort -- B200-native MSD radix sort of fixed-size records (RADULS2,
+arXiv 1703.00687, hot path).  The Python surface is a thin ctypes binding of
+libradsort.so; see include/radsort.h for the C ABI and DESIGN.md."""
+from .radsort import (  # noqa: F401
+    EXPORTS, LIB_PATH, RadsortError, finalize, init, last_stats, lib, locate_bucket, set_timing, sort, sort_host,
+    sort_multi, sort_ptr, version,
+)

@@ -1,0 +1,275 @@
+// radsort device code: the MSD radix-sort hot path for sm_100a.
+//
+// PAPER.md:35 §1 (MSD radix sort: partition by the most significant digit,
+// recurse into bins), §3.1 (1 B digits; whole-array pass,
+// then small bins, then tiny bins), §3.2 (small-bin counting
+// scatter; buffered, aligned scatter), §3.3 (tiny-bin
+// sorters; <=256-record bins skip empty/singleton sub-bins).  The GPU mapping
+// of each step is described in DESIGN.md §3 ("Kernels").
+//
+// Shares no code with oracle/ or datagen/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace radsort {
+
+constexpr int RADIX = 256;
+constexpr uint32_t TINY_MAX = 128;     // warp tiny sorter ceiling ("up to about a hundred")
+constexpr int TILE_BYTES = 65536;      // bytes per scatter/histogram tile
+constexpr int SCAT_B = 512;            // threads per scatter CTA
+constexpr int HIST_B = 256;            // threads per histogram CTA
+constexpr int LOCAL_B = 512;           // threads per CTA-local sorter
+constexpr int CHILD_B = 256;           // threads per children CTA
+constexpr int LOCAL_SMEM_BYTES = 131072;  // CTA-local sorter capacity in bytes
+
+template <int R> __host__ __device__ constexpr uint32_t tile_records() { return (uint32_t)(TILE_BYTES / R); }
+template <int R> __host__ __device__ constexpr uint32_t local_capacity() { return (uint32_t)(LOCAL_SMEM_BYTES / R); }
+
+enum : uint8_t { SRC_REC = 0, SRC_TMP = 1 };
+enum : uint8_t { MODE_NONE = 0, MODE_SCATTER = 1, MODE_COPY = 2 };
+enum : uint8_t { FLAG_EQUAL = 1 };
+
+// A bin ("bins that may be further processed independently"):
+// record range [off, off+len) of buffer `src`, to be partitioned by digit `depth`.
+struct Seg {
+  uint32_t off;
+  uint32_t len;
+  uint8_t depth;
+  uint8_t src;
+  uint8_t mode;
+  uint8_t flags;
+  uint32_t pad;
+};
+static_assert(sizeof(Seg) == 16, "Seg is 16 bytes");
+
+// Device-resident control block; the host reads it once per MSD level.
+struct Ctl {
+  uint32_t n_large_next;   // entries appended to Large[nxt] this level
+  uint32_t n_local[2];     // Local list counts (by parity)
+  uint32_t max_local_len[2];
+  uint32_t tiles_total;    // tiles of this level's Large list
+  uint32_t scatter_ticket; // decoupled look-back tile ticket
+  uint32_t d0;             // first digit of the level-0 pass (from k_sample)
+  unsigned long long rec_hist, rec_scatter, rec_copy, rec_tiny, rec_local, rec_final;
+  unsigned long long bins_large, bins_local, bins_tiny, bins_final;
+};
+
+// ------------------------------------------------------------------ records
+template <int R> struct Rec;
+template <> struct Rec<8> { uint2 a; };
+template <> struct Rec<16> { uint4 a; };
+template <> struct Rec<32> { uint4 a, b; };
+
+template <int R> __device__ __forceinline__ Rec<R> ld_rec(const uint8_t* p);
+template <> __device__ __forceinline__ Rec<8> ld_rec<8>(const uint8_t* p) { return {*reinterpret_cast<const uint2*>(p)}; }
+template <> __device__ __forceinline__ Rec<16> ld_rec<16>(const uint8_t* p) { return {*reinterpret_cast<const uint4*>(p)}; }
+template <> __device__ __forceinline__ Rec<32> ld_rec<32>(const uint8_t* p) {
+  return {reinterpret_cast<const uint4*>(p)[0], reinterpret_cast<const uint4*>(p)[1]};
+}
+template <int R> __device__ __forceinline__ void st_rec(uint8_t* p, const Rec<R>& r);
+template <> __device__ __forceinline__ void st_rec<8>(uint8_t* p, const Rec<8>& r) { *reinterpret_cast<uint2*>(p) = r.a; }
+template <> __device__ __forceinline__ void st_rec<16>(uint8_t* p, const Rec<16>& r) { *reinterpret_cast<uint4*>(p) = r.a; }
+template <> __device__ __forceinline__ void st_rec<32>(uint8_t* p, const Rec<32>& r) {
+  reinterpret_cast<uint4*>(p)[0] = r.a;
+  reinterpret_cast<uint4*>(p)[1] = r.b;
+}
+// read-only, non-coherent path for the streaming source of a pass
+template <int R> __device__ __forceinline__ Rec<R> ldg_rec(const uint8_t* p);
+template <> __device__ __forceinline__ Rec<8> ldg_rec<8>(const uint8_t* p) { return {__ldg(reinterpret_cast<const uint2*>(p))}; }
+template <> __device__ __forceinline__ Rec<16> ldg_rec<16>(const uint8_t* p) { return {__ldg(reinterpret_cast<const uint4*>(p))}; }
+template <> __device__ __forceinline__ Rec<32> ldg_rec<32>(const uint8_t* p) {
+  return {__ldg(reinterpret_cast<const uint4*>(p)), __ldg(reinterpret_cast<const uint4*>(p) + 1)};
+}
+
+__device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return (uint64_t)lo | ((uint64_t)hi << 32); }
+
+// ---------------------------------------------------------------------- keys
+// Key = bytes [0,K) as a little-endian unsigned integer (R1).
+template <int K> struct Key;
+template <> struct Key<8> { uint64_t w0; };
+template <> struct Key<16> { uint64_t w0, w1; };  // w1 = high word (bytes 8..15)
+
+template <int R, int K> __device__ __forceinline__ Key<K> key_of(const Rec<R>& r);
+template <> __device__ __forceinline__ Key<8> key_of<8, 8>(const Rec<8>& r) { return {u64of(r.a.x, r.a.y)}; }
+template <> __device__ __forceinline__ Key<8> key_of<16, 8>(const Rec<16>& r) { return {u64of(r.a.x, r.a.y)}; }
+template <> __device__ __forceinline__ Key<8> key_of<32, 8>(const Rec<32>& r) { return {u64of(r.a.x, r.a.y)}; }
+template <> __device__ __forceinline__ Key<16> key_of<16, 16>(const Rec<16>& r) { return {u64of(r.a.x, r.a.y), u64of(r.a.z, r.a.w)}; }
+template <> __device__ __forceinline__ Key<16> key_of<32, 16>(const Rec<32>& r) { return {u64of(r.a.x, r.a.y), u64of(r.a.z, r.a.w)}; }
+
+// Digit d, d = 0 most significant ("1 B digits"): byte K-1-d.
+__device__ __forceinline__ uint32_t digit_of(const Key<8>& k, uint32_t d) {
+  return (uint32_t)(k.w0 >> (8u * (7u - d))) & 255u;
+}
+__device__ __forceinline__ uint32_t digit_of(const Key<16>& k, uint32_t d) {
+  return d < 8 ? (uint32_t)(k.w1 >> (8u * (7u - d))) & 255u : (uint32_t)(k.w0 >> (8u * (15u - d))) & 255u;
+}
+
+// First digit >= d whose byte differs between the AND and the OR of all keys
+// of a bin (i.e. the first non-constant digit, "bins ... tend to
+// shrink (except bins with all keys equal)"); returns K if none.
+template <int K>
+__device__ __forceinline__ uint32_t first_nonconst_digit(const uint64_t* andw, const uint64_t* orw, uint32_t d) {
+  for (; d < (uint32_t)K; ++d) {
+    uint32_t bi = (uint32_t)K - 1u - d;
+    uint64_t x = (andw[bi >> 3] ^ orw[bi >> 3]) >> (8u * (bi & 7u));
+    if (x & 255u) return d;
+  }
+  return (uint32_t)K;
+}
+
+// ---------------------------------------------------------- status words
+// Decoupled look-back status (one per tile x digit): [63:48] epoch,
+// [47:46] flag (1 = tile aggregate, 2 = inclusive prefix), [45:0] value.
+constexpr uint64_t ST_AGG = 1ull << 46;
+constexpr uint64_t ST_PREFIX = 2ull << 46;
+constexpr uint64_t ST_VAL = (1ull << 46) - 1;
+
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ----------------------------------------------------------- block helpers
+// Exclusive scan of one value per thread for threads [0, 256); every thread
+// of the block must call it (it contains barriers).  `ws` = 8 words of smem.
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* ws) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t x = v;
+  if (tid < 256) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+  }
+  __syncthreads();
+  uint32_t add = 0;
+  if (tid < 256) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) add += (i < w) ? ws[i] : 0u;
+  }
+  __syncthreads();
+  return x - v + add;
+}
+
+// ------------------------------------------------------- warp tiny sorter
+// Sort key for a tiny bin at depth `depth` >= 1: the `depth` leading digits
+// are shared by the whole bin, so they are shifted out and the record's index
+// inside the bin (< 128, 7 bits) is packed into the freed low byte.  Ordering
+// the packed keys orders the records by key (ties by index), and the sort then
+// moves each full record once -- the enumeration-sort idea of "n assignments"
+// (§2.2, §3.3).
+struct SK8 {
+  uint64_t v;
+  __device__ __forceinline__ bool lt(const SK8& o) const { return v < o.v; }
+  __device__ __forceinline__ uint32_t idx() const { return (uint32_t)v & 255u; }
+  __device__ __forceinline__ SK8 shfl(int m) const { return {__shfl_xor_sync(0xffffffffu, v, m)}; }
+  static __device__ __forceinline__ SK8 maxv() { return {~0ull}; }
+};
+struct SK16 {
+  uint64_t hi, lo;
+  __device__ __forceinline__ bool lt(const SK16& o) const { return hi < o.hi || (hi == o.hi && lo < o.lo); }
+  __device__ __forceinline__ uint32_t idx() const { return (uint32_t)lo & 255u; }
+  __device__ __forceinline__ SK16 shfl(int m) const {
+    return {__shfl_xor_sync(0xffffffffu, hi, m), __shfl_xor_sync(0xffffffffu, lo, m)};
+  }
+  static __device__ __forceinline__ SK16 maxv() { return {~0ull, ~0ull}; }
+};
+template <int K> struct SKT;
+template <> struct SKT<8> { using T = SK8; };
+template <> struct SKT<16> { using T = SK16; };
+
+__device__ __forceinline__ SK8 make_sk(const Key<8>& k, uint32_t depth, uint32_t i) {
+  return {(k.w0 << (8u * depth)) | i};
+}
+__device__ __forceinline__ SK16 make_sk(const Key<16>& k, uint32_t depth, uint32_t i) {
+  const uint32_t s = 8u * depth;  // 8..120
+  uint64_t hi, lo;
+  if (s >= 64) { hi = k.w0 << (s - 64); lo = 0; }
+  else { hi = (k.w1 << s) | (k.w0 >> (64 - s)); lo = k.w0 << s; }
+  return {hi, lo | i};
+}
+
+// Bitonic sorting network over 32*E keys held E per lane (element i = lane*E+e),
+// PAPER.md:96-100 §2.2 (sorting networks: fixed comparators, hard-coded indices).
+template <class SK, int E>
+__device__ __forceinline__ void warp_bitonic(SK (&x)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = e ^ j;
+          if (p > e) {
+            const int i = lane * E + e;
+            const bool asc = (i & k) == 0;
+            SK a = x[e], b = x[p];
+            const bool sw = asc ? b.lt(a) : a.lt(b);
+            x[e] = sw ? b : a;
+            x[p] = sw ? a : b;
+          }
+        }
+      } else {
+        const int lm = j / E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane * E + e;
+          SK y = x[e].shfl(lm);
+          const bool takemin = (((i & j) == 0) == ((i & k) == 0));
+          const bool ylt = y.lt(x[e]);
+          x[e] = (takemin == ylt) ? y : x[e];
+        }
+      }
+    }
+  }
+}
+
+template <int R, int K, int E>
+__device__ __forceinline__ void tiny_sort_e(const uint8_t* src, uint8_t* dst, uint32_t n, uint32_t depth, int lane) {
+  using SK = typename SKT<K>::T;
+  SK x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(lane * E + e);
+    if (i < n) x[e] = make_sk(key_of<R, K>(ld_rec<R>(src + (size_t)i * R)), depth, i);
+    else x[e] = SK::maxv();
+  }
+  warp_bitonic<SK, E>(x, lane);
+  Rec<R> r[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(lane * E + e);
+    if (i < n) r[e] = ld_rec<R>(src + (size_t)x[e].idx() * R);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(lane * E + e);
+    if (i < n) st_rec<R>(dst + (size_t)i * R, r[e]);
+  }
+}
+
+// Sort a tiny bin of 2 <= n <= TINY_MAX records (one warp).  src and dst may
+// alias (every lane gathers before any lane stores) and may point into smem.
+template <int R, int K>
+__device__ __forceinline__ void warp_tiny_sort(const uint8_t* src, uint8_t* dst, uint32_t n, uint32_t depth, int lane) {
+  if (n <= 32) tiny_sort_e<R, K, 1>(src, dst, n, depth, lane);
+  else if (n <= 64) tiny_sort_e<R, K, 2>(src, dst, n, depth, lane);
+  else tiny_sort_e<R, K, 4>(src, dst, n, depth, lane);
+}
+
+template <int R>
+__device__ __forceinline__ void warp_copy(const uint8_t* src, uint8_t* dst, uint32_t n, int lane) {
+  for (uint32_t i = lane; i < n; i += 32) st_rec<R>(dst + (size_t)i * R, ld_rec<R>(src + (size_t)i * R));
+}
+
+}  // namespace radsort

@@ -1,0 +1,494 @@
+// radsort kernels: one MSD level = sample/hist -> plan -> scatter -> children,
+// plus the CTA-local sorter.  See DESIGN.md §3 for the roofline of each.
+#pragma once
+#include "kernels.cuh"
+
+namespace radsort {
+
+__device__ __forceinline__ uint8_t* buf_of(uint8_t src, uint8_t* recs, uint8_t* tmp) { return src == SRC_TMP ? tmp : recs; }
+
+// Index of the segment owning tile t: largest s with tile_start[s] <= t.
+__device__ __forceinline__ uint32_t seg_of_tile(const uint32_t* __restrict__ tile_start, uint32_t nseg, uint32_t t) {
+  uint32_t lo = 0, hi = nseg;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(tile_start + mid) <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// -------------------------------------------------------------- k_init
+// Level-0 set-up: the whole input is one bin.  If it fits the CTA-local
+// sorter it goes straight to the Local list, otherwise it becomes the single
+// Large segment of level 0 ("parallel processing of the whole
+// array according to the first digit").
+__global__ void k_init(Seg* large0, Seg* local0, Ctl* ctl, uint32_t n, uint32_t local_cap) {
+  Ctl c = {};
+  Seg s = {0u, n, 0, SRC_REC, MODE_NONE, 0, 0};
+  if (n <= local_cap) {
+    local0[0] = s;
+    c.n_local[0] = 1;
+    c.max_local_len[0] = n;
+  } else {
+    large0[0] = s;
+  }
+  *ctl = c;
+}
+
+// -------------------------------------------------------------- k_sample
+// Guess the first non-constant digit d0 from a strided sample (AND/OR of the
+// sampled keys).  A digit constant over the whole input is constant over any
+// sample, so the guess is never below the true d0; k_plan corrects it from
+// the full AND/OR if it was too high (one extra histogram read).
+template <int R, int K>
+__global__ void k_sample(Seg* large0, Ctl* ctl, const uint8_t* __restrict__ recs, uint32_t n) {
+  __shared__ unsigned long long sa[2], so[2];
+  constexpr int KW = K / 8;
+  if (threadIdx.x < 2) { sa[threadIdx.x] = ~0ull; so[threadIdx.x] = 0ull; }
+  __syncthreads();
+  uint64_t a[2] = {~0ull, ~0ull}, o[2] = {0ull, 0ull};
+  const uint32_t S = 4096;
+  const uint32_t stride = n > S ? n / S : 1;
+  for (uint32_t i = threadIdx.x; i < S && (uint64_t)i * stride < n; i += blockDim.x) {
+    Key<K> k = key_of<R, K>(ldg_rec<R>(recs + (size_t)i * stride * R));
+    a[0] &= k.w0; o[0] |= k.w0;
+    if constexpr (KW == 2) { a[1] &= k.w1; o[1] |= k.w1; }
+  }
+  for (int w = 0; w < KW; ++w) { atomicAnd(&sa[w], a[w]); atomicOr(&so[w], o[w]); }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t A[2] = {sa[0], sa[1]}, O[2] = {so[0], so[1]};
+    uint32_t d = first_nonconst_digit<K>(A, O, 0);
+    if (d >= (uint32_t)K) d = 0;
+    large0[0].depth = (uint8_t)d;
+    ctl->d0 = d;
+  }
+}
+
+// -------------------------------------------------------------- k_prep
+// Per level: tiles per Large segment -> exclusive prefix (single CTA), and
+// reset of the level's counters.
+__global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint32_t tile_recs, uint32_t* tile_start,
+                       Ctl* ctl, int nxt) {
+  __shared__ uint32_t ws[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const uint32_t per = (nseg + nt - 1) / nt;
+  const uint32_t b = tid * per, e = min(nseg, b + per);
+  uint32_t sum = 0;
+  for (uint32_t s = b; s < e; ++s) sum += (segs[s].len + tile_recs - 1) / tile_recs;
+  // block exclusive scan of `sum` (blockDim = 1024)
+  const int lane = tid & 31, w = tid >> 5;
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    ws[lane] = t;
+  }
+  __syncthreads();
+  uint32_t run = x - sum + (w > 0 ? ws[w - 1] : 0u);
+  for (uint32_t s = b; s < e; ++s) {
+    tile_start[s] = run;
+    run += (segs[s].len + tile_recs - 1) / tile_recs;
+  }
+  if (tid == nt - 1) {
+    tile_start[nseg] = run;
+    ctl->tiles_total = run;
+    ctl->scatter_ticket = 0;
+    ctl->n_large_next = 0;
+    ctl->n_local[nxt] = 0;
+    ctl->max_local_len[nxt] = 0;
+  }
+}
+
+// -------------------------------------------------------------- k_hist
+// Per-segment histogram of the segment's digit + AND/OR of its keys, one read
+// of the data ("counting sort may be applied per single phase").
+// Block-shared smem counters with atomics (measured ~10 atomics/clk/SM on
+// B200, ample for one digit per record).  andor[s] = {~AND words, OR words}
+// so that every accumulator starts at zero.
+template <int R, int K>
+__global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
+                                                 uint32_t nseg, const Ctl* __restrict__ ctl, uint32_t* __restrict__ hist,
+                                                 unsigned long long* __restrict__ andor, const uint8_t* recs,
+                                                 const uint8_t* tmp) {
+  constexpr uint32_t T = tile_records<R>();
+  constexpr int KW = K / 8;
+  __shared__ uint32_t h[RADIX];
+  const uint32_t total = ctl->tiles_total;
+  const int tid = threadIdx.x, lane = tid & 31;
+  unsigned long long cnt_recs = 0;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t s = seg_of_tile(tile_start, nseg, t);
+    const Seg sg = segs[s];
+    if (sg.flags & FLAG_EQUAL) continue;
+    const uint32_t lt = t - tile_start[s];
+    const uint32_t base = sg.off + lt * T;
+    const uint32_t m = min(T, sg.len - lt * T);
+    const uint8_t* src = (sg.src == SRC_TMP ? tmp : recs) + (size_t)base * R;
+    for (int i = tid; i < RADIX; i += HIST_B) h[i] = 0;
+    __syncthreads();
+    uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+    const uint32_t d = sg.depth;
+#pragma unroll 4
+    for (uint32_t i = tid; i < m; i += HIST_B) {
+      Key<K> k = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
+      atomicAdd(&h[digit_of(k, d)], 1u);
+      na[0] |= ~k.w0; o[0] |= k.w0;
+      if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+    }
+#pragma unroll
+    for (int w = 0; w < KW; ++w) {
+      uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+      uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+      uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+      uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+      if (lane == 0) {
+        atomicOr(&andor[(size_t)s * 4 + w], u64of(x0, x1));
+        atomicOr(&andor[(size_t)s * 4 + 2 + w], u64of(y0, y1));
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < RADIX; i += HIST_B)
+      if (h[i]) atomicAdd(&hist[(size_t)s * RADIX + i], h[i]);
+    cnt_recs += m;
+    __syncthreads();
+  }
+  if (tid == 0 && cnt_recs) atomicAdd((unsigned long long*)&ctl->rec_hist, cnt_recs);
+}
+
+// -------------------------------------------------------------- k_plan
+// Per Large segment: constant-digit skip / all-equal detection,
+// bin bases = exclusive prefix of the histogram.
+template <int K>
+__global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __restrict__ hist,
+                                                const unsigned long long* __restrict__ andor,
+                                                uint32_t* __restrict__ segbase, Seg* large_next, Ctl* ctl) {
+  __shared__ uint32_t ws[8];
+  __shared__ int sh_const;
+  const uint32_t s = blockIdx.x;
+  const int tid = threadIdx.x;
+  const Seg sg = segs[s];
+  if (sg.flags & FLAG_EQUAL) {  // known all-equal final bin: copy tmp -> records if needed
+    if (tid == 0) {
+      segs[s].mode = sg.src == SRC_TMP ? MODE_COPY : MODE_NONE;
+      atomicAdd(&ctl->rec_final, (unsigned long long)sg.len);
+    }
+    return;
+  }
+  if (tid == 0) sh_const = 0;
+  __syncthreads();
+  const uint32_t c = hist[(size_t)s * RADIX + tid];
+  if (c == sg.len) sh_const = 1;
+  __syncthreads();
+  if (sh_const) {
+    if (tid == 0) {
+      uint64_t A[2], O[2];
+      for (int w = 0; w < K / 8; ++w) { A[w] = ~andor[(size_t)s * 4 + w]; O[w] = andor[(size_t)s * 4 + 2 + w]; }
+      const uint32_t d2 = first_nonconst_digit<K>(A, O, sg.depth);
+      if (d2 >= (uint32_t)K) {  // all keys equal: final
+        segs[s].mode = sg.src == SRC_TMP ? MODE_COPY : MODE_NONE;
+        atomicAdd(&ctl->rec_final, (unsigned long long)sg.len);
+      } else {                  // skip constant digits, re-histogram next level
+        segs[s].mode = MODE_NONE;
+        Seg ns = sg;
+        ns.depth = (uint8_t)d2;
+        ns.mode = MODE_NONE;
+        large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+      }
+    }
+    return;
+  }
+  const uint32_t ex = block_excl_scan256(c, ws);
+  segbase[(size_t)s * RADIX + tid] = sg.off + ex;
+  if (tid == 0) segs[s].mode = MODE_SCATTER;
+}
+
+// -------------------------------------------------------------- k_scatter
+// One radix pass over every SCATTER segment of the level (§2.1
+// buffered scatter, §3.2): per tile, rank each record inside
+// its digit with shared-memory atomics, stage the tile in smem grouped by
+// digit, obtain each digit's global offset by single-pass decoupled look-back
+// over the segment's tiles, and write every digit run with coalesced stores.
+// Tiles come from an atomic ticket so look-back only waits on running CTAs.
+template <int R, int K>
+__global__ void __launch_bounds__(SCAT_B, 2) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
+                                                       uint32_t nseg, const uint32_t* __restrict__ segbase,
+                                                       unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
+                                                       uint8_t* recs, uint8_t* tmp) {
+  constexpr uint32_t T = tile_records<R>();
+  constexpr int I = (int)(T / SCAT_B);
+  extern __shared__ uint4 smem_raw[];
+  uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
+  __shared__ uint32_t cnt[RADIX], start[RADIX], gofs[RADIX], ws[8];
+  __shared__ uint32_t sh_t, sh_s;
+  const int tid = threadIdx.x;
+  const uint32_t total = ctl->tiles_total;
+  const uint64_t ep = (uint64_t)epoch << 48;
+  unsigned long long moved = 0;
+  for (;;) {
+    if (tid == 0) {
+      const uint32_t t = atomicAdd(&ctl->scatter_ticket, 1u);
+      sh_t = t;
+      if (t < total) sh_s = seg_of_tile(tile_start, nseg, t);
+    }
+    if (tid < RADIX) cnt[tid] = 0;
+    __syncthreads();
+    const uint32_t t = sh_t;
+    if (t >= total) break;
+    const uint32_t s = sh_s;
+    const Seg sg = segs[s];
+    if (sg.mode != MODE_NONE) {
+      const uint32_t lt = t - tile_start[s];
+      const uint32_t base = sg.off + lt * T;
+      const uint32_t m = min(T, sg.len - lt * T);
+      const uint8_t* src = buf_of(sg.src, recs, tmp);
+      uint8_t* dst = buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
+      if (sg.mode == MODE_COPY) {
+        for (uint32_t i = tid; i < m; i += SCAT_B)
+          st_rec<R>(dst + (size_t)(base + i) * R, ldg_rec<R>(src + (size_t)(base + i) * R));
+      } else {
+        const uint32_t d = sg.depth;
+        Rec<R> r[I];
+        uint32_t rk[I];
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const uint32_t idx = (uint32_t)(i * SCAT_B + tid);
+          if (idx < m) r[i] = ldg_rec<R>(src + (size_t)(base + idx) * R);
+        }
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const uint32_t idx = (uint32_t)(i * SCAT_B + tid);
+          if (idx < m) rk[i] = atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u);
+        }
+        __syncthreads();
+        uint32_t c = 0;
+        unsigned long long* my = status + (size_t)t * RADIX + tid;
+        if (tid < RADIX) {
+          c = cnt[tid];
+          st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
+        }
+        const uint32_t ex = block_excl_scan256(c, ws);
+        if (tid < RADIX) start[tid] = ex;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const uint32_t idx = (uint32_t)(i * SCAT_B + tid);
+          if (idx < m) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rk[i]) * R, r[i]);
+        }
+        if (tid < RADIX) {
+          uint64_t excl = 0;
+          if (lt > 0) {
+            const unsigned long long* p = status + (size_t)(t - 1) * RADIX + tid;
+            for (;;) {
+              const unsigned long long w = ld_relaxed(p);
+              if ((w & ~((1ull << 48) - 1)) != ep) continue;  // predecessor not published yet
+              excl += w & ST_VAL;
+              if (w & ST_PREFIX) break;
+              p -= RADIX;
+            }
+            st_relaxed(my, ep | ST_PREFIX | (excl + c));
+          }
+          gofs[tid] = segbase[(size_t)s * RADIX + tid] + (uint32_t)excl - ex;
+        }
+        __syncthreads();
+        for (uint32_t p = tid; p < m; p += SCAT_B) {
+          const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
+          const uint32_t dg = digit_of(key_of<R, K>(x), d);
+          st_rec<R>(dst + (size_t)(gofs[dg] + p) * R, x);
+        }
+      }
+      moved += m;
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && moved) atomicAdd(&ctl->rec_scatter, moved);
+}
+
+// -------------------------------------------------------------- k_children
+// Classify the 256 child bins of every scattered segment (PAPER.md:120-121
+// §3.1, §3.2): empty/singleton/all-equal ->
+// final (copied to the output buffer if they sit in tmp); <= TINY_MAX -> warp
+// tiny sort right here (§3.3); <= C -> Local list; larger ->
+// next level's Large list.
+template <int R, int K>
+__global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
+                                                      const uint32_t* __restrict__ segbase, Seg* large_next,
+                                                      Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
+  enum : uint8_t { C_NONE = 0, C_TINY = 1, C_COPY = 2 };
+  __shared__ uint8_t cls[RADIX];
+  __shared__ uint32_t coff[RADIX], clen[RADIX];
+  const uint32_t s = blockIdx.x;
+  const Seg sg = segs[s];
+  if (sg.mode != MODE_SCATTER) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint8_t loc = sg.src == SRC_TMP ? SRC_REC : SRC_TMP;  // children live where the scatter wrote
+  const uint32_t d1 = sg.depth + 1u;
+  constexpr uint32_t C = local_capacity<R>();
+  uint8_t* cbuf = buf_of(loc, recs, tmp);
+  if (tid < RADIX) {
+    const uint32_t len = hist[(size_t)s * RADIX + tid];
+    const uint32_t off = segbase[(size_t)s * RADIX + tid];
+    uint8_t c = C_NONE;
+    if (len == 0) {
+    } else if (d1 >= (uint32_t)K || len == 1) {  // all digits consumed / singleton: final
+      if (loc == SRC_TMP) {
+        if (len <= C) c = C_COPY;
+        else {
+          Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, FLAG_EQUAL, 0};
+          large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+        }
+      }
+      if (len <= C || loc != SRC_TMP) {
+        atomicAdd(&ctl->rec_final, (unsigned long long)len);
+        atomicAdd(&ctl->bins_final, 1ull);
+      }
+    } else if (len <= TINY_MAX) {
+      c = C_TINY;
+    } else if (len <= C) {
+      Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
+      local_cur[atomicAdd(&ctl->n_local[cur], 1u)] = ns;
+      atomicMax(&ctl->max_local_len[cur], len);
+      atomicAdd(&ctl->bins_local, 1ull);
+    } else {
+      Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
+      large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+      atomicAdd(&ctl->bins_large, 1ull);
+    }
+    cls[tid] = c;
+    coff[tid] = off;
+    clen[tid] = len;
+  }
+  __syncthreads();
+  unsigned long long tiny_recs = 0, tiny_bins = 0;
+  for (int v = warp; v < RADIX; v += CHILD_B / 32) {
+    const uint8_t c = cls[v];
+    if (c == C_NONE) continue;
+    const uint32_t off = coff[v], len = clen[v];
+    if (c == C_COPY) {
+      warp_copy<R>(cbuf + (size_t)off * R, recs + (size_t)off * R, len, lane);
+    } else {
+      warp_tiny_sort<R, K>(cbuf + (size_t)off * R, recs + (size_t)off * R, len, d1, lane);
+      tiny_recs += len;
+      tiny_bins += 1;
+    }
+  }
+  if (lane == 0 && tiny_bins) {
+    atomicAdd(&ctl->rec_tiny, tiny_recs);
+    atomicAdd(&ctl->bins_tiny, tiny_bins);
+  }
+}
+
+// -------------------------------------------------------------- k_local
+// CTA-local sort of a bin of <= C records (the GPU analog of PAPER.md:134
+// §3.2 "the bin is small enough to fit in a half of L2 ... simple counting
+// and scatter"): load the bin into registers, pick the first non-constant
+// digit from the block AND/OR (constant digits skipped),
+// counting-scatter it into shared memory, then finish every sub-bin from
+// smem: singletons / all-equal are copied, sub-bins <= TINY_MAX are sorted by
+// a warp (§3.3: only sub-bins with >= 2 records are visited
+// by a sorter), larger sub-bins are written out and queued for the next level.
+template <int R, int K, int IL>
+__global__ void __launch_bounds__(LOCAL_B) k_local(const Seg* __restrict__ list, Seg* local_next, int nxt, Ctl* ctl,
+                                                   uint8_t* recs, uint8_t* tmp) {
+  extern __shared__ uint4 smem_raw[];
+  uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
+  __shared__ uint32_t cnt[RADIX], start[RADIX], ws[8];
+  __shared__ unsigned long long sna[2], so[2];
+  __shared__ uint32_t sh_d;
+  constexpr int KW = K / 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Seg sg = list[blockIdx.x];
+  const uint32_t n = sg.len;
+  const uint8_t* src = buf_of(sg.src, recs, tmp) + (size_t)sg.off * R;
+  uint8_t* out = recs + (size_t)sg.off * R;
+  if (tid < RADIX) cnt[tid] = 0;
+  if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+  Rec<R> r[IL];
+  uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+#pragma unroll
+  for (int i = 0; i < IL; ++i) {
+    const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+    if (idx < n) {
+      r[i] = ldg_rec<R>(src + (size_t)idx * R);
+      Key<K> k = key_of<R, K>(r[i]);
+      na[0] |= ~k.w0; o[0] |= k.w0;
+      if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < KW; ++w) {
+    uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+    uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+    uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+    uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+    if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
+    sh_d = first_nonconst_digit<K>(A, O, sg.depth);
+  }
+  __syncthreads();
+  const uint32_t d = sh_d;
+  if (d >= (uint32_t)K) {  // all keys equal: final
+    if (sg.src == SRC_TMP) {
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        if (idx < n) st_rec<R>(out + (size_t)idx * R, r[i]);
+      }
+    }
+    if (tid == 0) atomicAdd(&ctl->rec_final, (unsigned long long)n);
+    return;
+  }
+  uint32_t rk[IL];
+#pragma unroll
+  for (int i = 0; i < IL; ++i) {
+    const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+    if (idx < n) rk[i] = atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u);
+  }
+  __syncthreads();
+  const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
+  const uint32_t ex = block_excl_scan256(c, ws);
+  if (tid < RADIX) start[tid] = ex;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IL; ++i) {
+    const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+    if (idx < n) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rk[i]) * R, r[i]);
+  }
+  __syncthreads();
+  const uint32_t d1 = d + 1;
+  for (int v = warp; v < RADIX; v += LOCAL_B / 32) {
+    const uint32_t len = cnt[v];
+    if (len == 0) continue;
+    const uint32_t o0 = start[v];
+    if (len == 1 || d1 >= (uint32_t)K) {
+      warp_copy<R>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, lane);
+    } else if (len <= TINY_MAX) {
+      warp_tiny_sort<R, K>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, d1, lane);
+    } else {
+      warp_copy<R>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, lane);
+      if (lane == 0) {
+        Seg ns = {sg.off + o0, len, (uint8_t)d1, SRC_REC, MODE_NONE, 0, 0};
+        local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
+        atomicMax(&ctl->max_local_len[nxt], len);
+      }
+    }
+  }
+  if (tid == 0) atomicAdd(&ctl->rec_local, (unsigned long long)n);
+}
+
+}  // namespace radsort

@@ -1,0 +1,170 @@
+"""Thin Python binding of libradsort.so (include/radsort.h).
+
+Argument marshalling only: every step of the sort runs in the library's CUDA
+kernels.  torch is used for device memory, streams and process groups.  There
+is no CPU fallback -- if the extension is missing, importing this module
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libradsort.so")
+
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_NOT_INITIALIZED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_CAPACITY = range(8)
+KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "multi"]
+
+# every symbol include/radsort.h declares
+EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
+           "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
+           "radsort_version"]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64), ("rec_size", ctypes.c_uint32), ("key_size", ctypes.c_uint32),
+        ("levels", ctypes.c_uint32), ("scatter_passes", ctypes.c_uint32),
+        ("constant_digits_skipped", ctypes.c_uint32), ("first_digit", ctypes.c_uint32),
+        ("records_scattered", ctypes.c_uint64), ("records_hist", ctypes.c_uint64),
+        ("records_local", ctypes.c_uint64), ("records_tiny", ctypes.c_uint64),
+        ("records_copied", ctypes.c_uint64),
+        ("bins_large", ctypes.c_uint64), ("bins_local", ctypes.c_uint64), ("bins_tiny", ctypes.c_uint64),
+        ("bins_final", ctypes.c_uint64),
+        ("nvlink_bytes_sent", ctypes.c_uint64), ("nvlink_bytes_recv", ctypes.c_uint64),
+        ("kernel_launches", ctypes.c_uint32 * 7), ("kernel_ms", ctypes.c_float * 7),
+        ("kernel_bytes", ctypes.c_uint64 * 7),
+    ]
+
+
+class RadsortError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"radsort status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                          "(radsort has no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    vp, u64, u32, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+    L.radsort_init.argtypes = [i32]
+    L.radsort_sort.argtypes = [vp, vp, u64, u32, u32, vp]
+    L.radsort_sort_host.argtypes = [vp, u64, u32, u32, vp]
+    L.radsort_sort_multi.argtypes = [vp, vp, u64, u64, ctypes.POINTER(u64), u32, u32, vp, vp]
+    L.radsort_locate_bucket.argtypes = [vp, u64, ctypes.POINTER(u32), ctypes.POINTER(u64)]
+    L.radsort_set_timing.argtypes = [i32]
+    L.radsort_last_stats.argtypes = [ctypes.POINTER(Stats)]
+    L.radsort_error_string.argtypes = [i32]
+    L.radsort_error_string.restype = ctypes.c_char_p
+    L.radsort_finalize.argtypes = []
+    L.radsort_finalize.restype = None
+    L.radsort_version.restype = ctypes.c_char_p
+    for f in ("radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
+              "radsort_set_timing", "radsort_last_stats"):
+        getattr(L, f).restype = i32
+    return L
+
+
+lib = _load()
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise RadsortError(rc, lib.radsort_error_string(rc).decode())
+
+
+def version() -> str:
+    return lib.radsort_version().decode()
+
+
+def init(device: int | None = None) -> None:
+    import torch
+
+    if device is None:
+        device = torch.cuda.current_device()
+    _check(lib.radsort_init(int(device)))
+
+
+def _stream_ptr(stream):
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def sort(records, tmp, key_size: int, stream=None, n: int | None = None) -> None:
+    """Sort records (a CUDA uint8 tensor of shape [n, R], contiguous) in place.
+    tmp: CUDA scratch tensor of >= n*R bytes (contents undefined afterwards)."""
+    assert records.is_cuda and tmp.is_cuda and records.is_contiguous() and tmp.is_contiguous()
+    R = records.shape[1] if records.dim() == 2 else int(records.numel() // (n or 1))
+    n = records.shape[0] if n is None else n
+    assert tmp.numel() * tmp.element_size() >= n * R, "tmp too small"
+    init(records.device.index)
+    _check(lib.radsort_sort(ctypes.c_void_p(records.data_ptr()), ctypes.c_void_p(tmp.data_ptr()), n, R, key_size,
+                            _stream_ptr(stream)))
+
+
+def sort_ptr(records_ptr: int, tmp_ptr: int, n: int, rec_size: int, key_size: int, stream_ptr: int = 0) -> None:
+    _check(lib.radsort_sort(ctypes.c_void_p(records_ptr), ctypes.c_void_p(tmp_ptr), n, rec_size, key_size,
+                            ctypes.c_void_p(stream_ptr)))
+
+
+def sort_host(records, key_size: int, stream=None) -> None:
+    """End-to-end sort of a host (ideally pinned) uint8 tensor/array [n, R] in place."""
+    import numpy as np
+
+    if isinstance(records, np.ndarray):
+        ptr, n, R = records.ctypes.data, records.shape[0], records.shape[1]
+    else:
+        ptr, n, R = records.data_ptr(), records.shape[0], records.shape[1]
+    _check(lib.radsort_sort_host(ctypes.c_void_p(ptr), n, R, key_size, _stream_ptr(stream)))
+
+
+def sort_multi(records, tmp, n_local: int, key_size: int, group=None, stream=None) -> int:
+    """Collective multi-GPU sort (one process per GPU); returns this rank's n_out."""
+    import torch
+    import torch.distributed as dist
+
+    group = group or dist.group.WORLD
+    backend = group._get_backend(torch.device("cuda"))
+    comm = backend._comm_ptr()
+    R = records.shape[1]
+    cap = min(records.shape[0], tmp.numel() * tmp.element_size() // R)
+    n_out = ctypes.c_uint64(0)
+    init(records.device.index)
+    _check(lib.radsort_sort_multi(ctypes.c_void_p(records.data_ptr()), ctypes.c_void_p(tmp.data_ptr()), n_local, cap,
+                                  ctypes.byref(n_out), R, key_size, ctypes.c_void_p(comm), _stream_ptr(stream)))
+    return int(n_out.value)
+
+
+def locate_bucket(hist256, q: int):
+    import numpy as np
+
+    h = np.ascontiguousarray(hist256, dtype=np.uint64)
+    assert h.shape == (256,)
+    b = ctypes.c_uint32(0)
+    before = ctypes.c_uint64(0)
+    _check(lib.radsort_locate_bucket(ctypes.c_void_p(h.ctypes.data), q, ctypes.byref(b), ctypes.byref(before)))
+    return int(b.value), int(before.value)
+
+
+def set_timing(on: bool) -> None:
+    _check(lib.radsort_set_timing(1 if on else 0))
+
+
+def last_stats() -> dict:
+    s = Stats()
+    _check(lib.radsort_last_stats(ctypes.byref(s)))
+    d = {k: getattr(s, k) for k, _ in Stats._fields_ if k not in ("kernel_launches", "kernel_ms", "kernel_bytes")}
+    d["kernel_launches"] = {c: int(s.kernel_launches[i]) for i, c in enumerate(KERNEL_CLASSES)}
+    d["kernel_ms"] = {c: float(s.kernel_ms[i]) for i, c in enumerate(KERNEL_CLASSES)}
+    d["kernel_bytes"] = {c: int(s.kernel_bytes[i]) for i, c in enumerate(KERNEL_CLASSES)}
+    return d
+
+
+def finalize() -> None:
+    lib.radsort_finalize()

@@ -1,0 +1,79 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/radsort.h declares, and its pure host functions behave."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "radsort.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(radsort_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    import paper_1703_00687_b200 as rs
+
+    lib = ctypes.CDLL(rs.LIB_PATH)
+    declared = header_functions()
+    assert "radsort_sort" in declared and "radsort_sort_multi" in declared and "radsort_init" in declared
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(rs.EXPORTS) == declared
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    import paper_1703_00687_b200 as rs
+
+    out = subprocess.run(["cuobjdump", "--list-elf", rs.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_errors():
+    import paper_1703_00687_b200 as rs
+
+    assert "radsort" in rs.version()
+    for s in range(8):
+        assert rs.lib.radsort_error_string(s)
+
+
+def test_locate_bucket_host_logic():
+    import paper_1703_00687_b200 as rs
+
+    h = np.zeros(256, dtype=np.uint64)
+    h[3], h[7], h[255] = 5, 10, 1
+    assert rs.locate_bucket(h, 0) == (3, 0)
+    assert rs.locate_bucket(h, 4) == (3, 0)
+    assert rs.locate_bucket(h, 5) == (7, 5)
+    assert rs.locate_bucket(h, 14) == (7, 5)
+    assert rs.locate_bucket(h, 15) == (255, 15)
+    with pytest.raises(rs.RadsortError):
+        rs.locate_bucket(h, 16)
+
+
+def test_bad_layouts_rejected_before_any_device_work():
+    import paper_1703_00687_b200 as rs
+    from paper_1703_00687_b200.radsort import ERR_INVALID_ARG, ERR_UNSUPPORTED
+
+    L = rs.lib
+    assert L.radsort_sort(None, None, 10, 8, 16, None) == ERR_INVALID_ARG   # K > R
+    assert L.radsort_sort(None, None, 10, 12, 8, None) == ERR_INVALID_ARG   # R not multiple of 8
+    assert L.radsort_sort(None, None, 10, 24, 8, None) == ERR_UNSUPPORTED   # not built yet
+    assert L.radsort_sort(None, None, 10, 8, 4, None) == ERR_INVALID_ARG
+
+
+def test_product_does_not_import_oracle():
+    # the product path never routes through the oracle (no CPU fallback)
+    pkg = os.path.join(ROOT, "paper_1703_00687_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in txt.replace("oracle/", ""), f

@@ -1,0 +1,149 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Every case: seeded synthetic input -> radsort_sort on cuda:0 -> copy back ->
+oracle.compare(gpu, oracle.sort(input)) == -1 (identical key sequence and
+identical record multiset inside every equal-key run).  Sizes span several
+tiles, ragged tails, every size-class boundary (tiny <= 128, local capacity
+C, tile T) and the degenerate distributions.  Red zones around both buffers
+check write containment (SPEC.md:318/331 analog)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from datagen import host as dg  # noqa: E402
+
+LAYOUTS = [(8, 8), (16, 8), (16, 16), (32, 8), (32, 16)]
+GUARD = 4096
+POISON = 0xA5
+
+
+def C_of(R):
+    return 131072 // R
+
+
+def T_of(R):
+    return 65536 // R
+
+
+def run_gpu_sort(a: np.ndarray, K: int, guard=True):
+    import paper_1703_00687_b200 as rs
+
+    n, R = a.shape
+    nb = n * R
+    dev = torch.device("cuda", 0)
+    big = torch.full((GUARD + max(nb, 16) + GUARD,), POISON, dtype=torch.uint8, device=dev)
+    big2 = torch.full((GUARD + max(nb, 16) + GUARD,), POISON, dtype=torch.uint8, device=dev)
+    rec = big[GUARD:GUARD + nb]
+    tmp = big2[GUARD:GUARD + max(nb, 16)]
+    if nb:
+        rec.copy_(torch.from_numpy(a.reshape(-1)))
+    rs.sort_ptr(rec.data_ptr(), tmp.data_ptr(), n, R, K, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    if guard:
+        for b, size in ((big, nb), (big2, max(nb, 16))):
+            assert bool((b[:GUARD] == POISON).all()), "write below buffer"
+            assert bool((b[GUARD + size:] == POISON).all()), "write above buffer"
+    return rec.cpu().numpy().reshape(n, R)
+
+
+def check(a, K):
+    got = run_gpu_sort(a, K)
+    want = oracle.sort(a, K)
+    bad = oracle.compare(got, want, K)
+    assert bad == -1, f"mismatch at record {bad} (n={a.shape[0]}, R={a.shape[1]}, K={K})"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    import paper_1703_00687_b200 as rs
+
+    rs.init(0)
+    yield
+
+
+@pytest.mark.parametrize("R,K", LAYOUTS)
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 31, 32, 33, 64, 65, 127, 128, 129, 255, 256, 257, 1000, 4097])
+def test_small_sizes(R, K, n):
+    check(dg.generate(n, R, K, "uniform", seed=1000 + n), K)
+
+
+@pytest.mark.parametrize("R,K", LAYOUTS)
+def test_capacity_and_tile_boundaries(R, K):
+    C, T = C_of(R), T_of(R)
+    for n in (C - 1, C, C + 1, T - 1, T + 1, 3 * T + 17):
+        check(dg.generate(n, R, K, "uniform", seed=n), K)
+
+
+@pytest.mark.parametrize("R,K", LAYOUTS)
+@pytest.mark.parametrize("dist", ["uniform", "uniform40", "zipf", "equal", "sorted", "reverse", "few", "consttop",
+                                  "bytes"])
+def test_distributions(R, K, dist):
+    for n in (5000, 300_000):
+        payload = "index" if R > K else "random"
+        check(dg.generate(n, R, K, dist, payload=payload, seed=77), K)
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (32, 16)])
+def test_multi_level_large(R, K):
+    # several Large levels, many tiles per segment, ragged tails everywhere
+    n = 2_000_003 if R <= 16 else 1_000_003
+    check(dg.generate(n, R, K, "uniform", seed=5), K)
+    check(dg.generate(n // 2, R, K, "bytes", seed=6), K)
+
+
+def test_c1_full_size_against_oracle():
+    a = dg.generate_config("c1")
+    check(a, 8)
+
+
+def test_repeated_calls_and_streams():
+    import paper_1703_00687_b200 as rs
+
+    a = dg.generate(100_000, 16, 8, "few", payload="index", seed=3)
+    want = oracle.sort(a, 8)
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        rec = torch.from_numpy(a.copy()).cuda()
+        tmp = torch.empty_like(rec)
+        with torch.cuda.stream(s):
+            rs.sort(rec, tmp, 8)
+        s.synchronize()
+        assert oracle.compare(rec.cpu().numpy(), want, 8) == -1
+
+
+def test_sort_host_end_to_end():
+    import paper_1703_00687_b200 as rs
+
+    a = dg.generate(300_000, 32, 16, "uniform", seed=9)
+    h = torch.from_numpy(a.copy()).pin_memory()
+    rs.sort_host(h, 16)
+    assert oracle.compare(h.numpy(), oracle.sort(a, 16), 16) == -1
+
+
+def test_device_datagen_matches_host_mirror():
+    from datagen import device as dd
+
+    for dist in ("uniform", "uniform40", "equal", "sorted", "reverse", "few", "consttop", "bytes"):
+        for R, K in ((8, 8), (16, 8), (32, 16)):
+            h = dg.generate(4099, R, K, dist, payload="index", seed=42, first=123)
+            d = dd.generate_tensor(4099, R, K, dist, payload="index", seed=42, first=123).cpu().numpy()
+            assert np.array_equal(h, d), (dist, R, K)
+    # Zipf: double-precision log/exp on both sides; allow a vanishing ulp-level disagreement
+    h = dg.generate(200_000, 8, 8, "zipf", seed=3)
+    d = dd.generate_tensor(200_000, 8, 8, "zipf", seed=3).cpu().numpy()
+    assert (h != d).any(axis=1).mean() < 1e-4
+
+
+def test_stats_report_constant_digit_skip():
+    import paper_1703_00687_b200 as rs
+
+    a = dg.generate_config("c2", n=1_000_000)
+    got = run_gpu_sort(a, 8, guard=False)
+    st = rs.last_stats()
+    assert st["first_digit"] == 3            # digits 0..2 constant (keys < 2^40)
+    w = got.view(np.uint64).reshape(-1, 2)
+    assert np.all(w[1:, 0] >= w[:-1, 0])
+    assert np.array_equal(np.sort(w[:, 1]), np.arange(1_000_000, dtype=np.uint64))

@@ -190,3 +190,14 @@ def test_compare_canonical():
     bad2 = want.copy()
     bad2[[j, j + 1]] = bad2[[j + 1, j]]
     assert oracle.compare(bad2, want, 8) == j
+
+
+def test_rank_bounds_against_sorted_positions():
+    a = dg.generate(5000, 16, 8, "few", payload="index", seed=8)
+    s = oracle.sort(a, 8)
+    keys = s.view(np.uint64).reshape(-1, 2)[:, 0]
+    for i in (0, 1, 77, 2500, 4999):
+        lt, le = oracle.rank_bounds(a, 8, s[i])
+        assert lt == int(np.searchsorted(keys, keys[i], "left"))
+        assert le == int(np.searchsorted(keys, keys[i], "right"))
+        assert lt <= i < le
