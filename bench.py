@@ -1,0 +1,338 @@
+#!/usr/bin/env python3
+"""radsort benchmark: sorted Mrecords/s and effective HBM GB/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl radsort|reference]
+
+A step = one radsort_sort of the whole workload (every MSD level: histogram,
+plan, look-back scatter, children/tiny, CTA-local sort) with the input already
+resident in HBM.  Between steps the input is restored from a pristine device
+copy (untimed; each step is bracketed by a barrier + cudaDeviceSynchronize and
+timed with CUDA events on the sort's stream).  Inputs (>= 3.2 GB at the
+default config) are larger than the 126 MB L2, so no L2 flush is needed.
+
+N = 1 runs the workload of BASELINE.json configs[1] (c2: 200M x 16 B records,
+8 B key < 2^40, payload = index) unless --config says otherwise.  N > 1
+(torchrun, one process per GPU, NCCL) runs radsort_sort_multi on a per-GPU
+shard of the same recipe (weak scaling: --config's n records per GPU).
+
+--impl reference times the CPU oracle (std::stable_sort, test infrastructure)
+on bounded samples of the same workload on the host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted Mrecords/s and effective HBM GB/s vs ~8 TB/s peak at 1/2/4/8 B200"
+UNIT = "Mrecords/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_desc(name, c, n):
+    return (f"{name}: {n} records, R={c['R']} B, K={c['K']} B, keys {c['dist']}, payload {c['payload']}, "
+            f"seed {c['seed']}")
+
+
+def cpu_baseline(cfg_name, target_s=10.0, max_n=40_000_000):
+    """The oracle as it stands (single-threaded std::stable_sort) on a bounded
+    prefix sample of the workload; returns (Mrecords/s, sample description)."""
+    import numpy as np
+
+    import oracle
+    from datagen import host as dg
+
+    c = dg.CONFIGS[cfg_name]
+    n = 1_000_000
+    a = dg.generate_config(cfg_name, n=n)
+    t0 = time.perf_counter()
+    oracle.sort(a, c["K"])
+    dt = time.perf_counter() - t0
+    n2 = int(min(max_n, max(n, n * target_s / max(dt, 1e-6))))
+    if n2 > n:
+        a = dg.generate_config(cfg_name, n=n2)
+        t0 = time.perf_counter()
+        oracle.sort(a, c["K"])
+        dt = time.perf_counter() - t0
+        n = n2
+    del np
+    return n / dt / 1e6, f"first {n} records of the {cfg_name} stream, oracle std::stable_sort, {dt:.2f} s"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from datagen import host as dg
+
+    import oracle
+
+    c = dg.CONFIGS[args.config]
+    # bounded sample per step (~5 s of CPU work), the same recipe as the GPU arm
+    n = args.ref_sample
+    a = dg.generate_config(args.config, n=n)
+    for _ in range(args.warmup):
+        oracle.sort(a, c["K"])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sort(a, c["K"])
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    v = args.steps * n / total / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config, c, c["n"]), "sample_records_per_step": n},
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {n} records of the {args.config} stream per step, std::stable_sort"},
+        "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_radsort(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1703_00687_b200 as rs
+    from datagen import device as dd
+    from datagen import host as dg
+    import verify
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    rs.init(local_rank)
+    c = dict(dg.CONFIGS[args.config])
+    n = args.n or c["n"]
+    R, K = c["R"], c["K"]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # input shard of this rank: global record indices [rank*n, (rank+1)*n)
+    pristine = dd.generate_tensor(n, R, K, c["dist"], c["payload"], c["seed"], first=rank * n)
+    cap = n if world == 1 else int(n * 1.0) + 1024
+    rec = torch.empty((cap, R), dtype=torch.uint8, device="cuda")
+    tmp = torch.empty((cap, R), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    dig_in = verify.digest(pristine.data_ptr(), n, R)
+
+    def restore():
+        rec[:n].copy_(pristine)
+
+    def one_sort():
+        if world == 1:
+            rs.sort_ptr(rec.data_ptr(), tmp.data_ptr(), n, R, K, stream.cuda_stream)
+            return n
+        return rs.sort_multi(rec, tmp, n, K)
+
+    # warm-up (the first one is also the verification run: sorted + same multiset)
+    for w in range(max(args.warmup, 1)):
+        restore()
+        torch.cuda.synchronize()
+        n_out = one_sort()
+        torch.cuda.synchronize()
+        if w == 0:
+            bad, first = verify.sorted_check(rec.data_ptr(), n_out, R, K)
+            if bad or (world == 1 and verify.digest(rec.data_ptr(), n, R) != dig_in):
+                print(json.dumps({"error": f"verification failed: {bad} inversions (first at {first})"}), flush=True)
+                return 1
+
+    rs.set_timing(True)
+    kern_ms = {}
+    kern_bytes = {}
+    launches = 0
+    step_ms = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            restore()
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            one_sort()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            step_ms.append(ev0.elapsed_time(ev1))
+            st = rs.last_stats()
+            for k, v in st["kernel_ms"].items():
+                kern_ms[k] = kern_ms.get(k, 0.0) + v
+            for k, v in st["kernel_bytes"].items():
+                kern_bytes[k] = kern_bytes.get(k, 0) + v
+            launches += sum(st["kernel_launches"].values())
+    rs.set_timing(False)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    stats = rs.last_stats()
+    N_total = n * world
+    value = N_total * args.steps / (total_ms / 1e3) / 1e6
+    passes_bytes = sum(kern_bytes.values()) / args.steps  # algorithmic bytes per step (read + write)
+    eff_gbs = passes_bytes * world / (total_ms / args.steps / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    sc_ms = kern_ms.get("scatter", 0.0)
+    sc_bytes = kern_bytes.get("scatter", 0)
+    achieved = sc_bytes / (sc_ms / 1e3) / 1e9 if sc_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("scatter_bytes_per_launch")
+
+    # end to end through the public C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host_pristine = pristine.cpu().pin_memory()
+        host = torch.empty_like(host_pristine).pin_memory()
+        e2e_t = []
+        for i in range(args.e2e_steps + 1):
+            host.copy_(host_pristine)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rs.sort_host(host, K)
+            dt = time.perf_counter() - t0
+            if i > 0:
+                e2e_t.append(dt)
+        e2e = {"value": round(n / statistics.median(e2e_t) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": n * R, "d2h_bytes_per_step": n * R}
+        del host, host_pristine
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample = cpu_baseline(args.config)
+        cpu = {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, c, n), "records_per_gpu": n, "rec_size": R,
+                       "key_size": K, "parallelism": f"key-range sharding x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than the 126 MB L2; input restored from a pristine copy between steps"},
+            "effective_hbm_gbs": round(eff_gbs, 1),
+            "hbm_frac_of_8tbs": round(eff_gbs / 8000.0, 4),
+            "roofline": {"bound": "hbm", "kernel": "k_scatter (look-back radix pass)",
+                         "achieved": round(achieved, 1) if achieved else None, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+                         "bytes_per_step": sc_bytes / args.steps, "ms_per_step": sc_ms / args.steps},
+            "kernel_ms_per_step": {k: round(v / args.steps, 4) for k, v in kern_ms.items()},
+            "kernel_bytes_per_step": {k: v // args.steps for k, v in kern_bytes.items()},
+            "passes": {"levels": stats["levels"], "scatter_passes": stats["scatter_passes"],
+                       "first_digit": stats["first_digit"]},
+            "gpu_launches": launches // args.steps,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--n", type=int, default=0, help="override records per GPU")
+    ap.add_argument("--impl", default="radsort", choices=["radsort", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_radsort(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

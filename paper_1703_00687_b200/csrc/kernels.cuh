@@ -272,4 +272,141 @@ __device__ __forceinline__ void warp_copy(const uint8_t* src, uint8_t* dst, uint
   for (uint32_t i = lane; i < n; i += 32) st_rec<R>(dst + (size_t)i * R, ld_rec<R>(src + (size_t)i * R));
 }
 
+__device__ __forceinline__ bool key_lt(const Key<8>& a, const Key<8>& b) { return a.w0 < b.w0; }
+__device__ __forceinline__ bool key_lt(const Key<16>& a, const Key<16>& b) {
+  return a.w1 < b.w1 || (a.w1 == b.w1 && a.w0 < b.w0);
+}
+
+// Lane-serial insertion sort of c (<= 8) records in place (§2.2,
+// PAPER.md:177 §3.3 insertion sort as the fix-up stage).
+template <int R, int K>
+__device__ __forceinline__ void lane_insertion_sort(uint8_t* base, uint32_t c) {
+  for (uint32_t i = 1; i < c; ++i) {
+    const Rec<R> x = ld_rec<R>(base + (size_t)i * R);
+    const Key<K> kx = key_of<R, K>(x);
+    int j = (int)i - 1;
+    for (; j >= 0; --j) {
+      const Rec<R> y = ld_rec<R>(base + (size_t)j * R);
+      if (!key_lt(kx, key_of<R, K>(y))) break;
+      st_rec<R>(base + (size_t)(j + 1) * R, y);
+    }
+    st_rec<R>(base + (size_t)(j + 1) * R, x);
+  }
+}
+
+template <int R, int K> __device__ __forceinline__ Key<K> ld_key(const uint8_t* p);
+template <> __device__ __forceinline__ Key<8> ld_key<8, 8>(const uint8_t* p) { return {*reinterpret_cast<const uint64_t*>(p)}; }
+template <> __device__ __forceinline__ Key<8> ld_key<16, 8>(const uint8_t* p) { return {*reinterpret_cast<const uint64_t*>(p)}; }
+template <> __device__ __forceinline__ Key<8> ld_key<32, 8>(const uint8_t* p) { return {*reinterpret_cast<const uint64_t*>(p)}; }
+template <> __device__ __forceinline__ Key<16> ld_key<16, 16>(const uint8_t* p) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  return {u64of(v.x, v.y), u64of(v.z, v.w)};
+}
+template <> __device__ __forceinline__ Key<16> ld_key<32, 16>(const uint8_t* p) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  return {u64of(v.x, v.y), u64of(v.z, v.w)};
+}
+__device__ __forceinline__ bool key_eq(const Key<8>& a, const Key<8>& b) { return a.w0 == b.w0; }
+__device__ __forceinline__ bool key_eq(const Key<16>& a, const Key<16>& b) { return a.w0 == b.w0 && a.w1 == b.w1; }
+
+// Enumeration-sort rank of record i inside bin [base, base+c) (PAPER.md:102-104
+// §2.2 "the final position of each element is determined by comparing it
+// against each other ... the number of element moves is only O(n)"; ties by
+// index): #{j: key_j < key_i} + #{j < i: key_j == key_i}.
+template <int R, int K>
+__device__ __forceinline__ uint32_t es_rank(const uint8_t* base, uint32_t c, uint32_t i, const Key<K>& ki) {
+  uint32_t rank = 0;
+  for (uint32_t j = 0; j < c; ++j) {
+    const Key<K> kj = ld_key<R, K>(base + (size_t)j * R);
+    rank += (key_lt(kj, ki) || (j < i && key_eq(kj, ki))) ? 1u : 0u;
+  }
+  return rank;
+}
+
+// Enumeration-sort ceiling: bins of 2..ES_MAX records are finished record-
+// parallel by es_rank (§3.3: ES for the tiniest bins, and
+// for wider records up to 24); larger tiny bins use warp_tail_sort.
+template <int R> __host__ __device__ constexpr uint32_t es_max() { return R >= 32 ? 24u : 16u; }
+
+// Per-warp scratch of the tail sorter (shared memory).
+template <int K>
+struct TailScratch {
+  uint32_t cnt[RADIX];      // digit counters, then packed (start << 16 | count)
+  Key<K> key[TINY_MAX];     // keys in partitioned order
+};
+
+// Tail sorter for a bin of 2 <= n <= TINY_MAX records, one warp (PAPER.md
+// §3.3, GPU form).  One counting pass on digit `depth` with warp-private smem
+// counters (sub-bins holding a single record are final and
+// never visited again); every record of a sub-bin with c >= 2 records gets its
+// place by enumeration sort among those c records only (PAPER.md:102-104 ES:
+// n comparisons, one move per record; ties by partition slot).  Works on keys;
+// each full record is then moved once, src -> out.  src and out must not alias.
+template <int R, int K>
+__device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
+                                               TailScratch<K>& ws) {
+  constexpr int E = TINY_MAX / 32;
+  uint4* w4 = reinterpret_cast<uint4*>(ws.cnt);
+  w4[lane * 2] = make_uint4(0, 0, 0, 0);
+  w4[lane * 2 + 1] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  Key<K> k[E];
+  uint32_t pr[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(e * 32 + lane);
+    if (e * 32 < (int)n && i < n) {
+      k[e] = ld_key<R, K>(src + (size_t)i * R);
+      pr[e] = atomicAdd(&ws.cnt[digit_of(k[e], depth)], 1u);
+    }
+  }
+  __syncwarp();
+  {
+    const uint4 c0 = w4[lane * 2], c1 = w4[lane * 2 + 1];
+    const uint32_t tot = c0.x + c0.y + c0.z + c0.w + c1.x + c1.y + c1.z + c1.w;
+    uint32_t inc = tot;
+#pragma unroll
+    for (int sft = 1; sft < 32; sft <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, sft);
+      if (lane >= sft) inc += y;
+    }
+    const uint32_t r0 = inc - tot;
+    const uint32_t r1 = r0 + c0.x, r2 = r1 + c0.y, r3 = r2 + c0.z, r4 = r3 + c0.w;
+    const uint32_t r5 = r4 + c1.x, r6 = r5 + c1.y, r7 = r6 + c1.z;
+    __syncwarp();
+    w4[lane * 2] = make_uint4((r0 << 16) | c0.x, (r1 << 16) | c0.y, (r2 << 16) | c0.z, (r3 << 16) | c0.w);
+    w4[lane * 2 + 1] = make_uint4((r4 << 16) | c1.x, (r5 << 16) | c1.y, (r6 << 16) | c1.z, (r7 << 16) | c1.w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(e * 32 + lane);
+    if (e * 32 < (int)n && i < n) {
+      const uint32_t w = ws.cnt[digit_of(k[e], depth)];
+      const uint32_t slot = (w >> 16) + pr[e];
+      ws.key[slot] = k[e];
+      pr[e] = slot | ((w >> 16) << 8) | ((w & 0xffffu) << 16);  // slot | start << 8 | count << 16
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(e * 32 + lane);
+    if (e * 32 < (int)n && i < n) {
+      const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
+      uint32_t fin = slot;
+      if (c > 1) {
+        uint32_t r = 0;
+        for (uint32_t q = s0; q < s0 + c; ++q) {
+          const Key<K> kq = ws.key[q];
+          r += (key_lt(kq, k[e]) || (q < slot && key_eq(kq, k[e]))) ? 1u : 0u;
+        }
+        fin = s0 + r;
+      }
+      st_rec<R>(out + (size_t)fin * R, ld_rec<R>(src + (size_t)i * R));
+    }
+  }
+  __syncwarp();
+}
+
 }  // namespace radsort

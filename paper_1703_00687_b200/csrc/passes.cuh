@@ -22,7 +22,7 @@ __device__ __forceinline__ uint32_t seg_of_tile(const uint32_t* __restrict__ til
 // sorter it goes straight to the Local list, otherwise it becomes the single
 // Large segment of level 0 ("parallel processing of the whole
 // array according to the first digit").
-__global__ void k_init(Seg* large0, Seg* local0, Ctl* ctl, uint32_t n, uint32_t local_cap) {
+static __global__ void k_init(Seg* large0, Seg* local0, Ctl* ctl, uint32_t n, uint32_t local_cap) {
   Ctl c = {};
   Seg s = {0u, n, 0, SRC_REC, MODE_NONE, 0, 0};
   if (n <= local_cap) {
@@ -68,7 +68,7 @@ __global__ void k_sample(Seg* large0, Ctl* ctl, const uint8_t* __restrict__ recs
 // -------------------------------------------------------------- k_prep
 // Per level: tiles per Large segment -> exclusive prefix (single CTA), and
 // reset of the level's counters.
-__global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint32_t tile_recs, uint32_t* tile_start,
+static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint32_t tile_recs, uint32_t* tile_start,
                        Ctl* ctl, int nxt) {
   __shared__ uint32_t ws[32];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -114,9 +114,11 @@ __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint32_t til
 // -------------------------------------------------------------- k_hist
 // Per-segment histogram of the segment's digit + AND/OR of its keys, one read
 // of the data ("counting sort may be applied per single phase").
-// Block-shared smem counters with atomics (measured ~10 atomics/clk/SM on
-// B200, ample for one digit per record).  andor[s] = {~AND words, OR words}
-// so that every accumulator starts at zero.
+// Each CTA owns a contiguous range of tiles and accumulates in shared memory
+// (smem atomics: measured ~10/clk/SM on B200, ample for one digit per record)
+// until the segment changes, so global atomics are per CTA and segment, not per
+// tile.  andor[s] = {OR of ~key words, OR of key words}: all accumulators start
+// at zero.
 template <int R, int K>
 __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                  uint32_t nseg, const Ctl* __restrict__ ctl, uint32_t* __restrict__ hist,
@@ -124,46 +126,76 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
                                                  const uint8_t* tmp) {
   constexpr uint32_t T = tile_records<R>();
   constexpr int KW = K / 8;
+  constexpr int U = 8;  // keys in flight per thread
   __shared__ uint32_t h[RADIX];
+  __shared__ unsigned long long sna[2], so[2];
   const uint32_t total = ctl->tiles_total;
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * per, t1 = min(total, t0 + per);
+  if (t0 >= t1) return;
   const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < RADIX; i += HIST_B) h[i] = 0;
+  if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+  __syncthreads();
+  uint64_t na[2] = {0, 0}, o[2] = {0, 0};
   unsigned long long cnt_recs = 0;
-  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
-    const uint32_t s = seg_of_tile(tile_start, nseg, t);
-    const Seg sg = segs[s];
-    if (sg.flags & FLAG_EQUAL) continue;
-    const uint32_t lt = t - tile_start[s];
-    const uint32_t base = sg.off + lt * T;
-    const uint32_t m = min(T, sg.len - lt * T);
-    const uint8_t* src = (sg.src == SRC_TMP ? tmp : recs) + (size_t)base * R;
-    for (int i = tid; i < RADIX; i += HIST_B) h[i] = 0;
-    __syncthreads();
-    uint64_t na[2] = {0, 0}, o[2] = {0, 0};
-    const uint32_t d = sg.depth;
-#pragma unroll 4
-    for (uint32_t i = tid; i < m; i += HIST_B) {
-      Key<K> k = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
-      atomicAdd(&h[digit_of(k, d)], 1u);
-      na[0] |= ~k.w0; o[0] |= k.w0;
-      if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
-    }
+  uint32_t cur = seg_of_tile(tile_start, nseg, t0);
+  uint32_t cur_end = tile_start[cur + 1];
+  auto flush = [&](uint32_t s) {
 #pragma unroll
     for (int w = 0; w < KW; ++w) {
-      uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
-      uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
-      uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
-      uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
-      if (lane == 0) {
-        atomicOr(&andor[(size_t)s * 4 + w], u64of(x0, x1));
-        atomicOr(&andor[(size_t)s * 4 + 2 + w], u64of(y0, y1));
-      }
+      const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+      const uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+      const uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+      const uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+      if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
+      na[w] = 0;
+      o[w] = 0;
     }
     __syncthreads();
-    for (int i = tid; i < RADIX; i += HIST_B)
+    for (int i = tid; i < RADIX; i += HIST_B) {
       if (h[i]) atomicAdd(&hist[(size_t)s * RADIX + i], h[i]);
-    cnt_recs += m;
+      h[i] = 0;
+    }
+    if (tid < KW) {
+      if (sna[tid]) atomicOr(&andor[(size_t)s * 4 + tid], sna[tid]);
+      if (so[tid]) atomicOr(&andor[(size_t)s * 4 + 2 + tid], so[tid]);
+    }
     __syncthreads();
+    if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+  };
+  for (uint32_t t = t0; t < t1; ++t) {
+    if (t >= cur_end) {
+      flush(cur);
+      cur = seg_of_tile(tile_start, nseg, t);
+      cur_end = tile_start[cur + 1];
+    }
+    const Seg sg = segs[cur];
+    if (sg.flags & FLAG_EQUAL) continue;
+    const uint32_t lt = t - tile_start[cur];
+    const uint32_t m = min(T, sg.len - lt * T);
+    const uint8_t* src = (sg.src == SRC_TMP ? tmp : recs) + (size_t)(sg.off + lt * T) * R;
+    const uint32_t d = sg.depth;
+    for (uint32_t i0 = tid; i0 < m; i0 += HIST_B * U) {
+      Key<K> k[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + u * HIST_B;
+        if (i < m) k[u] = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + u * HIST_B;
+        if (i < m) {
+          atomicAdd(&h[digit_of(k[u], d)], 1u);
+          na[0] |= ~k[u].w0; o[0] |= k[u].w0;
+          if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
+        }
+      }
+    }
+    cnt_recs += m;
   }
+  flush(cur);
   if (tid == 0 && cnt_recs) atomicAdd((unsigned long long*)&ctl->rec_hist, cnt_recs);
 }
 
@@ -318,20 +350,24 @@ __global__ void __launch_bounds__(SCAT_B, 2) k_scatter(const Seg* __restrict__ s
 // -------------------------------------------------------------- k_children
 // Classify the 256 child bins of every scattered segment (PAPER.md:120-121
 // §3.1, §3.2): empty/singleton/all-equal ->
-// final (copied to the output buffer if they sit in tmp); <= TINY_MAX -> warp
-// tiny sort right here (§3.3); <= C -> Local list; larger ->
-// next level's Large list.
+// final (copied to the output buffer if they sit in tmp); 2..ES_MAX records ->
+// enumeration sort right here; <= TINY_MAX -> warp small-bin sorter right here
+// (§3.3); <= C -> Local list; larger -> next level's Large
+// list.  Dynamic smem: one TINY_MAX*R scratch per warp.
 template <int R, int K>
 __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
                                                       Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
-  enum : uint8_t { C_NONE = 0, C_TINY = 1, C_COPY = 2 };
+  enum : uint8_t { C_NONE = 0, C_COPY = 1, C_ES = 2, C_TINY = 3 };
+  extern __shared__ uint4 smem_raw[];
   __shared__ uint8_t cls[RADIX];
   __shared__ uint32_t coff[RADIX], clen[RADIX];
+  __shared__ __align__(16) TailScratch<K> wsc[CHILD_B / 32];
   const uint32_t s = blockIdx.x;
   const Seg sg = segs[s];
   if (sg.mode != MODE_SCATTER) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* scratch = reinterpret_cast<uint8_t*>(smem_raw) + (size_t)warp * TINY_MAX * R;
   const uint8_t loc = sg.src == SRC_TMP ? SRC_REC : SRC_TMP;  // children live where the scatter wrote
   const uint32_t d1 = sg.depth + 1u;
   constexpr uint32_t C = local_capacity<R>();
@@ -353,6 +389,8 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
         atomicAdd(&ctl->rec_final, (unsigned long long)len);
         atomicAdd(&ctl->bins_final, 1ull);
       }
+    } else if (len <= es_max<R>()) {
+      c = C_ES;
     } else if (len <= TINY_MAX) {
       c = C_TINY;
     } else if (len <= C) {
@@ -375,10 +413,28 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
     const uint8_t c = cls[v];
     if (c == C_NONE) continue;
     const uint32_t off = coff[v], len = clen[v];
+    const uint8_t* src = cbuf + (size_t)off * R;
+    uint8_t* out = recs + (size_t)off * R;
     if (c == C_COPY) {
-      warp_copy<R>(cbuf + (size_t)off * R, recs + (size_t)off * R, len, lane);
+      warp_copy<R>(src, out, len, lane);
+    } else if (c == C_ES) {
+      Rec<R> x;
+      uint32_t rank = 0;
+      if ((uint32_t)lane < len) {
+        x = ld_rec<R>(src + (size_t)lane * R);
+        rank = es_rank<R, K>(src, len, (uint32_t)lane, key_of<R, K>(x));
+      }
+      __syncwarp();
+      if ((uint32_t)lane < len) st_rec<R>(out + (size_t)rank * R, x);
+      tiny_recs += len;
+      tiny_bins += 1;
     } else {
-      warp_tiny_sort<R, K>(cbuf + (size_t)off * R, recs + (size_t)off * R, len, d1, lane);
+      if (src == out) {  // in place: stage the bin in the warp's smem scratch first
+        warp_copy<R>(src, scratch, len, lane);
+        __syncwarp();
+        src = scratch;
+      }
+      warp_tail_sort<R, K>(src, out, len, d1, lane, wsc[warp]);
       tiny_recs += len;
       tiny_bins += 1;
     }
@@ -390,105 +446,163 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
 }
 
 // -------------------------------------------------------------- k_local
-// CTA-local sort of a bin of <= C records (the GPU analog of PAPER.md:134
+// CTA-local sort of bins of <= C records (the GPU analog of PAPER.md:134
 // §3.2 "the bin is small enough to fit in a half of L2 ... simple counting
-// and scatter"): load the bin into registers, pick the first non-constant
-// digit from the block AND/OR (constant digits skipped),
-// counting-scatter it into shared memory, then finish every sub-bin from
-// smem: singletons / all-equal are copied, sub-bins <= TINY_MAX are sorted by
-// a warp (§3.3: only sub-bins with >= 2 records are visited
-// by a sorter), larger sub-bins are written out and queued for the next level.
+// and scatter").  Persistent CTAs walk the Local list; for each bin: records
+// in registers -> block AND/OR picks the first non-constant digit (constant
+// digits skipped) -> counting scatter into shared memory -> the
+// bin after next is prefetched into L2 by a TMA bulk prefetch -> every sub-bin is
+// finished from smem by one warp: singletons / all-equal copied, <= TINY_MAX
+// sorted by warp_tail_sort (§3.3), larger ones written out
+// and queued for the next level.
 template <int R, int K, int IL>
-__global__ void __launch_bounds__(LOCAL_B) k_local(const Seg* __restrict__ list, Seg* local_next, int nxt, Ctl* ctl,
-                                                   uint8_t* recs, uint8_t* tmp) {
+__global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t stage_bytes,
+                                                      Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
-  __shared__ uint32_t cnt[RADIX], start[RADIX], ws[8];
+  __shared__ uint32_t cnt[RADIX], start[RADIX], ws[8], big[RADIX];
   __shared__ unsigned long long sna[2], so[2];
-  __shared__ uint32_t sh_d;
+  __shared__ uint32_t sh_d, nbig;
   constexpr int KW = K / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Seg sg = list[blockIdx.x];
-  const uint32_t n = sg.len;
-  const uint8_t* src = buf_of(sg.src, recs, tmp) + (size_t)sg.off * R;
-  uint8_t* out = recs + (size_t)sg.off * R;
+  TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(stage + stage_bytes)[warp];
+  uint32_t bi = blockIdx.x;
+  if (bi >= nlist) return;
+  Seg sg = list[bi];
+  Rec<R> r[IL];
+  auto load = [&](const Seg& g) {
+    const uint8_t* src = buf_of(g.src, recs, tmp) + (size_t)g.off * R;
+#pragma unroll
+    for (int i = 0; i < IL; ++i) {
+      const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+      if (idx < g.len) r[i] = ldg_rec<R>(src + (size_t)idx * R);
+    }
+  };
+  auto prefetch_l2 = [&](uint32_t b) {  // TMA bulk prefetch of a whole bin into L2
+    if (tid == 0 && b < nlist) {
+      const Seg g = list[b];
+      const uintptr_t s0 = (uintptr_t)(buf_of(g.src, recs, tmp) + (size_t)g.off * R);
+      const uintptr_t e0 = s0 + (size_t)g.len * R;
+      const uintptr_t s1 = (s0 + 15) & ~(uintptr_t)15, e1 = e0 & ~(uintptr_t)15;
+      if (e1 > s1)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s1), "r"((uint32_t)(e1 - s1)) : "memory");
+    }
+  };
+  prefetch_l2(bi + gridDim.x);
   if (tid < RADIX) cnt[tid] = 0;
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-  Rec<R> r[IL];
-  uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+  if (tid == 0) nbig = 0;
+  unsigned long long done = 0;
+  for (;;) {
+    const uint32_t n = sg.len;
+    uint8_t* out = recs + (size_t)sg.off * R;
+    load(sg);
+    uint64_t na[2] = {0, 0}, o[2] = {0, 0};
 #pragma unroll
-  for (int i = 0; i < IL; ++i) {
-    const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
-    if (idx < n) {
-      r[i] = ldg_rec<R>(src + (size_t)idx * R);
-      Key<K> k = key_of<R, K>(r[i]);
-      na[0] |= ~k.w0; o[0] |= k.w0;
-      if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+    for (int i = 0; i < IL; ++i) {
+      const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+      if (idx < n) {
+        const Key<K> k = key_of<R, K>(r[i]);
+        na[0] |= ~k.w0; o[0] |= k.w0;
+        if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+      }
     }
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int w = 0; w < KW; ++w) {
-    uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
-    uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
-    uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
-    uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
-    if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
-    sh_d = first_nonconst_digit<K>(A, O, sg.depth);
-  }
-  __syncthreads();
-  const uint32_t d = sh_d;
-  if (d >= (uint32_t)K) {  // all keys equal: final
-    if (sg.src == SRC_TMP) {
+    for (int w = 0; w < KW; ++w) {
+      const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+      const uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+      const uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+      const uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+      if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
+      sh_d = first_nonconst_digit<K>(A, O, sg.depth);
+    }
+    __syncthreads();
+    const uint32_t d = sh_d;
+    if (d >= (uint32_t)K) {  // all keys equal: final where it is (copied out of tmp)
+      if (sg.src == SRC_TMP) {
+#pragma unroll
+        for (int i = 0; i < IL; ++i) {
+          const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+          if (idx < n) st_rec<R>(out + (size_t)idx * R, r[i]);
+        }
+      }
+    } else {
+      constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
+      uint32_t rk[IP];
+#pragma unroll
+      for (int i = 0; i < IP; ++i) rk[i] = 0;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
-        if (idx < n) st_rec<R>(out + (size_t)idx * R, r[i]);
+        if (idx < n) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u) << (16 * (i & 1));
+      }
+      __syncthreads();
+      const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
+      if (tid < RADIX && c > es_max<R>()) big[atomicAdd(&nbig, 1u)] = tid;  // sub-bins for phase B
+      const uint32_t ex = block_excl_scan256(c, ws);
+      if (tid < RADIX) start[tid] = ex;
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        const uint32_t rki = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+        if (idx < n) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rki) * R, r[i]);
+      }
+      __syncthreads();
+    }
+    // the bin after next streams into L2 while this one is finished from smem
+    const uint32_t nb = bi + gridDim.x;
+    prefetch_l2(nb + gridDim.x);
+    if (d < (uint32_t)K) {
+      const uint32_t d1 = d + 1;
+      // phase A, record-parallel: singletons / exhausted digits copied, sub-bins
+      // of 2..ES_MAX records finished by enumeration sort
+      for (uint32_t p = tid; p < n; p += LOCAL_B) {
+        const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
+        const Key<K> kx = key_of<R, K>(x);
+        const uint32_t v = digit_of(kx, d), c = cnt[v];
+        if (c == 1 || d1 >= (uint32_t)K) {
+          st_rec<R>(out + (size_t)p * R, x);
+        } else if (c <= es_max<R>()) {
+          const uint32_t s0 = start[v];
+          st_rec<R>(out + (size_t)(s0 + es_rank<R, K>(stage + (size_t)s0 * R, c, p - s0, kx)) * R, x);
+        }
+      }
+      // phase B, one warp per larger sub-bin
+      if (d1 < (uint32_t)K) {
+        const uint32_t nb_ = nbig;
+        for (uint32_t q = warp; q < nb_; q += LOCAL_B / 32) {
+          const uint32_t v = big[q];
+          const uint32_t len = cnt[v];
+          const uint32_t o0 = start[v];
+          if (len <= TINY_MAX) {
+            warp_tail_sort<R, K>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, d1, lane, tsc);
+          } else {
+            warp_copy<R>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, lane);
+            if (lane == 0) {
+              Seg ns = {sg.off + o0, len, (uint8_t)d1, SRC_REC, MODE_NONE, 0, 0};
+              local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
+              atomicMax(&ctl->max_local_len[nxt], len);
+            }
+          }
+        }
       }
     }
-    if (tid == 0) atomicAdd(&ctl->rec_final, (unsigned long long)n);
-    return;
+    done += n;
+    __syncthreads();
+    if (tid < RADIX) cnt[tid] = 0;
+    if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+    if (tid == 0) nbig = 0;
+    if (nb >= nlist) break;
+    bi = nb;
+    sg = list[nb];
   }
-  uint32_t rk[IL];
-#pragma unroll
-  for (int i = 0; i < IL; ++i) {
-    const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
-    if (idx < n) rk[i] = atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u);
-  }
-  __syncthreads();
-  const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
-  const uint32_t ex = block_excl_scan256(c, ws);
-  if (tid < RADIX) start[tid] = ex;
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IL; ++i) {
-    const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
-    if (idx < n) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rk[i]) * R, r[i]);
-  }
-  __syncthreads();
-  const uint32_t d1 = d + 1;
-  for (int v = warp; v < RADIX; v += LOCAL_B / 32) {
-    const uint32_t len = cnt[v];
-    if (len == 0) continue;
-    const uint32_t o0 = start[v];
-    if (len == 1 || d1 >= (uint32_t)K) {
-      warp_copy<R>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, lane);
-    } else if (len <= TINY_MAX) {
-      warp_tiny_sort<R, K>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, d1, lane);
-    } else {
-      warp_copy<R>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, lane);
-      if (lane == 0) {
-        Seg ns = {sg.off + o0, len, (uint8_t)d1, SRC_REC, MODE_NONE, 0, 0};
-        local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
-        atomicMax(&ctl->max_local_len[nxt], len);
-      }
-    }
-  }
-  if (tid == 0) atomicAdd(&ctl->rec_local, (unsigned long long)n);
+  if (tid == 0) atomicAdd(&ctl->rec_local, done);
 }
 
 }  // namespace radsort

@@ -1,0 +1,196 @@
+// The MSD level loop for one record layout (instantiated in layout_R_K.cu).
+#pragma once
+#include "driver.cuh"
+
+namespace radsort {
+
+// -------------------------------------------------------------- the sort
+template <int R, int K>
+struct Sorter {
+  static constexpr uint32_t T = tile_records<R>();
+  static constexpr uint32_t C = local_capacity<R>();
+  static constexpr int LOCAL_SCRATCH = (LOCAL_B / 32) * (int)sizeof(TailScratch<K>);
+  static constexpr int LOCAL_DYN_MAX = LOCAL_SMEM_BYTES + LOCAL_SCRATCH;
+  static constexpr int CHILD_SCRATCH = (CHILD_B / 32) * (int)TINY_MAX * R;
+
+  template <int IL>
+  static void launch_local_t(uint32_t nloc, size_t stage_bytes, const Seg* list, Seg* next, int nxt, Ctl* ctl,
+                             uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+    const size_t smem = stage_bytes + LOCAL_SCRATCH;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_local<R, K, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, LOCAL_DYN_MAX);
+      attr = true;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL>, LOCAL_B, smem);
+    const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
+    k_local<R, K, IL><<<g, LOCAL_B, smem, st>>>(list, nloc, (uint32_t)stage_bytes, next, nxt, ctl, recs, tmp);
+  }
+
+  static void set_attrs() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_scatter<R, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_BYTES);
+    cudaFuncSetAttribute(k_children<R, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, CHILD_SCRATCH);
+    done = true;
+  }
+
+  // Local bins of up to `maxlen` records: IL = records per thread.
+  static void launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
+                           uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+    const uint32_t il = (maxlen + LOCAL_B - 1) / LOCAL_B;
+    const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
+#define RS_LOCAL(IL) launch_local_t<IL>(nloc, stage_bytes, list, next, nxt, ctl, recs, tmp, st, sms)
+    if (il <= 1) RS_LOCAL(1);
+    else if (il <= 2) RS_LOCAL(2);
+    else if (il <= 4) RS_LOCAL(4);
+    else if (il <= 8) RS_LOCAL(8);
+    else if constexpr (R <= 16) {
+      if (il <= 16) RS_LOCAL(16);
+      else if constexpr (R <= 8) RS_LOCAL(32);
+    }
+#undef RS_LOCAL
+  }
+
+  static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
+                            radsort_stats& stats) {
+    set_attrs();
+    // ---- workspace
+    const size_t capL = (size_t)n / C + 4;
+    const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4;
+    const size_t tiles_max = (size_t)n / T + capL + 4;
+    radsort_status rs;
+    if ((rs = ensure(ctx->large[0], capL * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->large[1], capL * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->local[0], capLoc * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->local[1], capLoc * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->hist, capL * RADIX * sizeof(uint32_t)))) return rs;
+    if ((rs = ensure(ctx->segbase, capL * RADIX * sizeof(uint32_t)))) return rs;
+    if ((rs = ensure(ctx->andor, capL * 4 * sizeof(unsigned long long)))) return rs;
+    if ((rs = ensure(ctx->tile_start, (capL + 1) * sizeof(uint32_t)))) return rs;
+    const size_t old_status = ctx->status.bytes;
+    if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
+    if (ctx->status.bytes != old_status) ctx->epoch = 0;
+    if ((rs = ensure(ctx->ctl, sizeof(Ctl)))) return rs;
+    if (!ctx->h_ctl) RS_CUDA(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
+
+    Seg* L[2] = {(Seg*)ctx->large[0].p, (Seg*)ctx->large[1].p};
+    Seg* Lo[2] = {(Seg*)ctx->local[0].p, (Seg*)ctx->local[1].p};
+    uint32_t* hist = (uint32_t*)ctx->hist.p;
+    uint32_t* segbase = (uint32_t*)ctx->segbase.p;
+    unsigned long long* andor = (unsigned long long*)ctx->andor.p;
+    uint32_t* tile_start = (uint32_t*)ctx->tile_start.p;
+    unsigned long long* status = (unsigned long long*)ctx->status.p;
+    Ctl* ctl = (Ctl*)ctx->ctl.p;
+
+    int occ_s = 0, occ_h = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K>, SCAT_B, TILE_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K>, HIST_B, 0);
+    occ_s = std::max(occ_s, 1);
+    occ_h = std::max(occ_h, 1);
+
+    Timer tm(ctx, st);
+    const bool log = getenv("RADSORT_LOG") && getenv("RADSORT_LOG")[0] == '1';
+
+    k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
+    uint32_t n_large = n > C ? 1u : 0u;
+    if (n_large) {
+      tm.begin(RADSORT_K_SAMPLE);
+      k_sample<R, K><<<1, 256, 0, st>>>(L[0], ctl, recs, n);
+      tm.end();
+      stats.kernel_launches[RADSORT_K_SAMPLE]++;
+    }
+    int cur = 0;
+    const int max_levels = 2 * K + 4;
+    for (int level = 0;; ++level) {
+      if (level > max_levels) {
+        set_detail("MSD level loop did not terminate (%d levels)", level);
+        return RADSORT_ERR_CUDA;
+      }
+      const int nxt = cur ^ 1;
+      if (n_large) {
+        RS_CUDA(cudaMemsetAsync(hist, 0, (size_t)n_large * RADIX * sizeof(uint32_t), st));
+        RS_CUDA(cudaMemsetAsync(andor, 0, (size_t)n_large * 4 * sizeof(unsigned long long), st));
+        tm.begin(RADSORT_K_PLAN);
+        k_prep<<<1, 1024, 0, st>>>(L[cur], n_large, T, tile_start, ctl, nxt);
+        tm.end();
+        const size_t tiles_ub = std::min(tiles_max, (size_t)n / T + n_large + 1);
+        const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
+        tm.begin(RADSORT_K_HIST);
+        k_hist<R, K><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
+        tm.end();
+        tm.begin(RADSORT_K_PLAN);
+        k_plan<K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl);
+        tm.end();
+        if (++ctx->epoch >= 65536) {
+          RS_CUDA(cudaMemsetAsync(status, 0, ctx->status.bytes, st));
+          ctx->epoch = 1;
+        }
+        const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
+        tm.begin(RADSORT_K_SCATTER);
+        k_scatter<R, K><<<gs, SCAT_B, TILE_BYTES, st>>>(L[cur], tile_start, n_large, segbase, status, ctx->epoch, ctl,
+                                                        recs, tmp);
+        tm.end();
+        tm.begin(RADSORT_K_CHILDREN);
+        k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs, tmp);
+        tm.end();
+        stats.kernel_launches[RADSORT_K_PLAN] += 2;
+        stats.kernel_launches[RADSORT_K_HIST]++;
+        stats.kernel_launches[RADSORT_K_SCATTER]++;
+        stats.kernel_launches[RADSORT_K_CHILDREN]++;
+        stats.scatter_passes++;
+      } else {
+        k_prep<<<1, 1024, 0, st>>>(L[cur], 0, T, tile_start, ctl, nxt);
+        stats.kernel_launches[RADSORT_K_PLAN]++;
+      }
+      RS_CUDA(cudaGetLastError());
+      RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaStreamSynchronize(st));
+      const Ctl c = *ctx->h_ctl;
+      if (level == 0) stats.first_digit = c.d0;
+      const uint32_t nloc = c.n_local[cur];
+      if (log)
+        fprintf(stderr, "[radsort] level %d: large=%u tiles=%u -> large_next=%u local=%u (max %u)\n", level, n_large,
+                c.tiles_total, c.n_large_next, nloc, c.max_local_len[cur]);
+      if (nloc) {
+        tm.begin(RADSORT_K_LOCAL);
+        launch_local(nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, ctl, recs, tmp, st, ctx->sms);
+        tm.end();
+        stats.kernel_launches[RADSORT_K_LOCAL]++;
+        RS_CUDA(cudaGetLastError());
+      }
+      stats.levels = level + 1;
+      tm.flush(stats);
+      if (c.n_large_next == 0 && nloc == 0 && n_large == 0) break;
+      n_large = c.n_large_next;
+      cur = nxt;
+    }
+    // final statistics (one more small read; the sort's last kernels are ordered before it)
+    RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    const Ctl c = *ctx->h_ctl;
+    stats.records_scattered = c.rec_scatter;
+    stats.records_hist = c.rec_hist;
+    stats.records_local = c.rec_local;
+    stats.records_tiny = c.rec_tiny;
+    stats.records_copied = c.rec_copy;
+    stats.bins_large = c.bins_large;
+    stats.bins_local = c.bins_local;
+    stats.bins_tiny = c.bins_tiny;
+    stats.bins_final = c.bins_final;
+    stats.kernel_bytes[RADSORT_K_HIST] = c.rec_hist * R;
+    stats.kernel_bytes[RADSORT_K_SCATTER] = 2ull * c.rec_scatter * R;
+    stats.kernel_bytes[RADSORT_K_LOCAL] = 2ull * c.rec_local * R;
+    stats.kernel_bytes[RADSORT_K_CHILDREN] = 2ull * c.rec_tiny * R;
+    return RADSORT_OK;
+  }
+};
+
+
+template <int R, int K>
+radsort_status run_layout(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st, radsort_stats& s) {
+  return Sorter<R, K>::run(ctx, recs, tmp, n, st, s);
+}
+
+}  // namespace radsort
