@@ -16,14 +16,11 @@ namespace radsort {
 
 constexpr int RADIX = 256;
 constexpr uint32_t TINY_MAX = 128;     // warp tiny sorter ceiling ("up to about a hundred")
-constexpr int TILE_BYTES = 65536;      // bytes per scatter/histogram tile
-constexpr int SCAT_B = 512;            // threads per scatter CTA
 constexpr int HIST_B = 256;            // threads per histogram CTA
 constexpr int LOCAL_B = 512;           // threads per CTA-local sorter
 constexpr int CHILD_B = 256;           // threads per children CTA
 constexpr int LOCAL_SMEM_BYTES = 131072;  // CTA-local sorter capacity in bytes
 
-template <int R> __host__ __device__ constexpr uint32_t tile_records() { return (uint32_t)(TILE_BYTES / R); }
 template <int R> __host__ __device__ constexpr uint32_t local_capacity() { return (uint32_t)(LOCAL_SMEM_BYTES / R); }
 
 enum : uint8_t { SRC_REC = 0, SRC_TMP = 1 };
@@ -53,6 +50,7 @@ struct Ctl {
   uint32_t d0;             // first digit of the level-0 pass (from k_sample)
   unsigned long long rec_hist, rec_scatter, rec_copy, rec_tiny, rec_local, rec_final;
   unsigned long long bins_large, bins_local, bins_tiny, bins_final;
+  unsigned long long prof[16];  // phase cycle counters (RADSORT_PHASE_PROF builds only)
 };
 
 // ------------------------------------------------------------------ records
@@ -133,6 +131,35 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+
+// ------------------------------------------------ TMA bulk copy / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared (16-byte aligned addresses, size % 16 == 0),
+// completion signalled on `bar` as transaction bytes.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// order this thread's earlier generic-proxy smem accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ----------------------------------------------------------- block helpers
 // Exclusive scan of one value per thread for threads [0, 256); every thread
@@ -274,7 +301,7 @@ __device__ __forceinline__ void warp_copy(const uint8_t* src, uint8_t* dst, uint
 
 __device__ __forceinline__ bool key_lt(const Key<8>& a, const Key<8>& b) { return a.w0 < b.w0; }
 __device__ __forceinline__ bool key_lt(const Key<16>& a, const Key<16>& b) {
-  return a.w1 < b.w1 || (a.w1 == b.w1 && a.w0 < b.w0);
+  return (a.w1 < b.w1) | ((a.w1 == b.w1) & (a.w0 < b.w0));
 }
 
 // Lane-serial insertion sort of c (<= 8) records in place (§2.2,
@@ -307,7 +334,7 @@ template <> __device__ __forceinline__ Key<16> ld_key<32, 16>(const uint8_t* p) 
   return {u64of(v.x, v.y), u64of(v.z, v.w)};
 }
 __device__ __forceinline__ bool key_eq(const Key<8>& a, const Key<8>& b) { return a.w0 == b.w0; }
-__device__ __forceinline__ bool key_eq(const Key<16>& a, const Key<16>& b) { return a.w0 == b.w0 && a.w1 == b.w1; }
+__device__ __forceinline__ bool key_eq(const Key<16>& a, const Key<16>& b) { return (a.w0 == b.w0) & (a.w1 == b.w1); }
 
 // Enumeration-sort rank of record i inside bin [base, base+c) (PAPER.md:102-104
 // §2.2 "the final position of each element is determined by comparing it
@@ -315,10 +342,19 @@ __device__ __forceinline__ bool key_eq(const Key<16>& a, const Key<16>& b) { ret
 // index): #{j: key_j < key_i} + #{j < i: key_j == key_i}.
 template <int R, int K>
 __device__ __forceinline__ uint32_t es_rank(const uint8_t* base, uint32_t c, uint32_t i, const Key<K>& ki) {
-  uint32_t rank = 0;
-  for (uint32_t j = 0; j < c; ++j) {
+  // branch-free accumulation (the paper's SETcc idea), 4 keys in flight
+  uint32_t rank = 0, j = 0;
+  for (; j + 4 <= c; j += 4) {
+    Key<K> kj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) kj[u] = ld_key<R, K>(base + (size_t)(j + u) * R);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      rank += (uint32_t)key_lt(kj[u], ki) | ((uint32_t)(j + u < i) & (uint32_t)key_eq(kj[u], ki));
+  }
+  for (; j < c; ++j) {
     const Key<K> kj = ld_key<R, K>(base + (size_t)j * R);
-    rank += (key_lt(kj, ki) || (j < i && key_eq(kj, ki))) ? 1u : 0u;
+    rank += (uint32_t)key_lt(kj, ki) | ((uint32_t)(j < i) & (uint32_t)key_eq(kj, ki));
   }
   return rank;
 }
@@ -342,10 +378,9 @@ struct TailScratch {
 // place by enumeration sort among those c records only (PAPER.md:102-104 ES:
 // n comparisons, one move per record; ties by partition slot).  Works on keys;
 // each full record is then moved once, src -> out.  src and out must not alias.
-template <int R, int K>
-__device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
-                                               TailScratch<K>& ws) {
-  constexpr int E = TINY_MAX / 32;
+template <int R, int K, int E>
+__device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
+                                                 TailScratch<K>& ws) {
   uint4* w4 = reinterpret_cast<uint4*>(ws.cnt);
   w4[lane * 2] = make_uint4(0, 0, 0, 0);
   w4[lane * 2 + 1] = make_uint4(0, 0, 0, 0);
@@ -355,7 +390,7 @@ __device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out,
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const uint32_t i = (uint32_t)(e * 32 + lane);
-    if (e * 32 < (int)n && i < n) {
+    if (i < n) {
       k[e] = ld_key<R, K>(src + (size_t)i * R);
       pr[e] = atomicAdd(&ws.cnt[digit_of(k[e], depth)], 1u);
     }
@@ -381,7 +416,7 @@ __device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out,
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const uint32_t i = (uint32_t)(e * 32 + lane);
-    if (e * 32 < (int)n && i < n) {
+    if (i < n) {
       const uint32_t w = ws.cnt[digit_of(k[e], depth)];
       const uint32_t slot = (w >> 16) + pr[e];
       ws.key[slot] = k[e];
@@ -392,14 +427,18 @@ __device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out,
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const uint32_t i = (uint32_t)(e * 32 + lane);
-    if (e * 32 < (int)n && i < n) {
+    if (i < n) {
       const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
       uint32_t fin = slot;
-      if (c > 1) {
+      if (c == 2) {  // the common collision: one comparison with the partner
+        const uint32_t other = 2 * s0 + 1 - slot;
+        const Key<K> kq = ws.key[other];
+        fin = s0 + ((uint32_t)key_lt(kq, k[e]) | ((uint32_t)(other < slot) & (uint32_t)key_eq(kq, k[e])));
+      } else if (c > 2) {
         uint32_t r = 0;
         for (uint32_t q = s0; q < s0 + c; ++q) {
           const Key<K> kq = ws.key[q];
-          r += (key_lt(kq, k[e]) || (q < slot && key_eq(kq, k[e]))) ? 1u : 0u;
+          r += (uint32_t)key_lt(kq, k[e]) | ((uint32_t)(q < slot) & (uint32_t)key_eq(kq, k[e]));
         }
         fin = s0 + r;
       }
@@ -407,6 +446,14 @@ __device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out,
     }
   }
   __syncwarp();
+}
+
+template <int R, int K>
+__device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
+                                               TailScratch<K>& ws) {
+  if (n <= 32) warp_tail_sort_e<R, K, 1>(src, out, n, depth, lane, ws);
+  else if (n <= 64) warp_tail_sort_e<R, K, 2>(src, out, n, depth, lane, ws);
+  else warp_tail_sort_e<R, K, 4>(src, out, n, depth, lane, ws);
 }
 
 }  // namespace radsort

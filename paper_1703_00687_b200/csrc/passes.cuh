@@ -119,12 +119,12 @@ static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint3
 // until the segment changes, so global atomics are per CTA and segment, not per
 // tile.  andor[s] = {OR of ~key words, OR of key words}: all accumulators start
 // at zero.
-template <int R, int K>
+template <int R, int K, int TB>
 __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                  uint32_t nseg, const Ctl* __restrict__ ctl, uint32_t* __restrict__ hist,
                                                  unsigned long long* __restrict__ andor, const uint8_t* recs,
                                                  const uint8_t* tmp) {
-  constexpr uint32_t T = tile_records<R>();
+  constexpr uint32_t T = (uint32_t)(TB / R);
   constexpr int KW = K / 8;
   constexpr int U = 8;  // keys in flight per thread
   __shared__ uint32_t h[RADIX];
@@ -253,13 +253,14 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __res
 // digit, obtain each digit's global offset by single-pass decoupled look-back
 // over the segment's tiles, and write every digit run with coalesced stores.
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
-template <int R, int K>
-__global__ void __launch_bounds__(SCAT_B, 2) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
+template <int R, int K, int TB, int SB, int MINB>
+__global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
                                                        uint8_t* recs, uint8_t* tmp) {
-  constexpr uint32_t T = tile_records<R>();
-  constexpr int I = (int)(T / SCAT_B);
+  constexpr uint32_t T = (uint32_t)(TB / R);
+  constexpr int I = (int)(T / SB);
+  constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
   __shared__ uint32_t cnt[RADIX], start[RADIX], gofs[RADIX], ws[8];
@@ -268,83 +269,140 @@ __global__ void __launch_bounds__(SCAT_B, 2) k_scatter(const Seg* __restrict__ s
   const uint32_t total = ctl->tiles_total;
   const uint64_t ep = (uint64_t)epoch << 48;
   unsigned long long moved = 0;
-  for (;;) {
-    if (tid == 0) {
-      const uint32_t t = atomicAdd(&ctl->scatter_ticket, 1u);
-      sh_t = t;
-      if (t < total) sh_s = seg_of_tile(tile_start, nseg, t);
-    }
-    if (tid < RADIX) cnt[tid] = 0;
-    __syncthreads();
-    const uint32_t t = sh_t;
-    if (t >= total) break;
-    const uint32_t s = sh_s;
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = 0, tB = 0;
+#define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
+#else
+#define RS_PROF(i) do { } while (0)
+#endif
+  // thread 0: take a ticket (the look-back forward-progress order) and find its segment
+  auto take = [&]() {
+    const uint32_t t = atomicAdd(&ctl->scatter_ticket, 1u);
+    sh_t = t;
+    sh_s = t < total ? seg_of_tile(tile_start, nseg, t) : 0u;
+  };
+  Rec<R> r[I];
+  // issue this tile's loads into r[] (software pipelining: the loads of tile
+  // k+1 are in flight while tile k is looked back and written out)
+  auto load = [&](uint32_t t, uint32_t s) {
     const Seg sg = segs[s];
-    if (sg.mode != MODE_NONE) {
-      const uint32_t lt = t - tile_start[s];
-      const uint32_t base = sg.off + lt * T;
-      const uint32_t m = min(T, sg.len - lt * T);
-      const uint8_t* src = buf_of(sg.src, recs, tmp);
-      uint8_t* dst = buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
-      if (sg.mode == MODE_COPY) {
-        for (uint32_t i = tid; i < m; i += SCAT_B)
-          st_rec<R>(dst + (size_t)(base + i) * R, ldg_rec<R>(src + (size_t)(base + i) * R));
-      } else {
-        const uint32_t d = sg.depth;
-        Rec<R> r[I];
-        uint32_t rk[I];
+    if (sg.mode != MODE_SCATTER) return;
+    const uint32_t lt = t - tile_start[s];
+    const uint32_t m = min(T, sg.len - lt * T);
+    const uint8_t* src = buf_of(sg.src, recs, tmp) + (size_t)(sg.off + lt * T) * R;
 #pragma unroll
-        for (int i = 0; i < I; ++i) {
-          const uint32_t idx = (uint32_t)(i * SCAT_B + tid);
-          if (idx < m) r[i] = ldg_rec<R>(src + (size_t)(base + idx) * R);
-        }
+    for (int i = 0; i < I; ++i) {
+      const uint32_t idx = (uint32_t)(i * SB + tid);
+      if (idx < m) r[i] = ldg_rec<R>(src + (size_t)idx * R);
+    }
+  };
+  if (tid == 0) take();
+  if (tid < RADIX) cnt[tid] = 0;
+  __syncthreads();
+  uint32_t t = sh_t, s = sh_s;
+  if (t < total) load(t, s);
+  while (t < total) {
+#ifdef RADSORT_PHASE_PROF
+    if (tid == 0) { tA = clock64(); pf[7]++; }
+#endif
+    const Seg sg = segs[s];
+    const uint32_t lt = t - tile_start[s];
+    const uint32_t base = sg.off + lt * T;
+    const uint32_t m = min(T, sg.len - lt * T);
+    uint8_t* dst = buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
+    if (sg.mode == MODE_SCATTER) {
+      const uint32_t d = sg.depth;
+      uint32_t rk[I];
 #pragma unroll
-        for (int i = 0; i < I; ++i) {
-          const uint32_t idx = (uint32_t)(i * SCAT_B + tid);
-          if (idx < m) rk[i] = atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u);
-        }
-        __syncthreads();
-        uint32_t c = 0;
-        unsigned long long* my = status + (size_t)t * RADIX + tid;
-        if (tid < RADIX) {
-          c = cnt[tid];
-          st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
-        }
-        const uint32_t ex = block_excl_scan256(c, ws);
-        if (tid < RADIX) start[tid] = ex;
-        __syncthreads();
+      for (int i = 0; i < I; ++i) {
+        const uint32_t idx = (uint32_t)(i * SB + tid);
+        if (idx < m) rk[i] = atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u);
+      }
+      __syncthreads();
+      RS_PROF(1);
+      uint32_t c = 0;
+      unsigned long long* my = status + (size_t)t * RADIX + tid;
+      if (tid < RADIX) {
+        c = cnt[tid];
+        st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
+      }
+      if (tid == 0) take();  // next ticket, ready before the stage barrier
+      const uint32_t ex = block_excl_scan256(c, ws);
+      if (tid < RADIX) start[tid] = ex;
+      __syncthreads();
+      RS_PROF(2);
 #pragma unroll
-        for (int i = 0; i < I; ++i) {
-          const uint32_t idx = (uint32_t)(i * SCAT_B + tid);
-          if (idx < m) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rk[i]) * R, r[i]);
-        }
-        if (tid < RADIX) {
-          uint64_t excl = 0;
-          if (lt > 0) {
-            const unsigned long long* p = status + (size_t)(t - 1) * RADIX + tid;
-            for (;;) {
-              const unsigned long long w = ld_relaxed(p);
-              if ((w & ~((1ull << 48) - 1)) != ep) continue;  // predecessor not published yet
-              excl += w & ST_VAL;
-              if (w & ST_PREFIX) break;
-              p -= RADIX;
+      for (int i = 0; i < I; ++i) {
+        const uint32_t idx = (uint32_t)(i * SB + tid);
+        if (idx < m) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rk[i]) * R, r[i]);
+      }
+      __syncthreads();  // r[] free, sh_t/sh_s hold the next ticket
+      const uint32_t tn = sh_t, sn = sh_s;
+      if (tid < RADIX) cnt[tid] = 0;
+      if (tn < total) load(tn, sn);
+      RS_PROF(3);
+      if (tid < RADIX) {
+        uint64_t excl = 0;
+        if (lt > 0) {
+          // windowed decoupled look-back over this segment's earlier tiles
+          uint32_t p = t - 1;
+          for (;;) {
+            unsigned long long w[LBW];
+#pragma unroll
+            for (int j = 0; j < LBW; ++j)
+              w[j] = (p >= (uint32_t)j) ? ld_relaxed(status + (size_t)(p - j) * RADIX + tid) : 0ull;
+            int j = 0;
+            bool done = false;
+#pragma unroll
+            for (int q = 0; q < LBW; ++q) {
+              if (done || j != q) continue;
+              if ((w[q] & ~((1ull << 48) - 1)) != ep) continue;  // not yet published: reload from here
+              excl += w[q] & ST_VAL;
+              if (w[q] & ST_PREFIX) done = true;
+              else j = q + 1;
             }
-            st_relaxed(my, ep | ST_PREFIX | (excl + c));
+            if (done) break;
+            p -= (uint32_t)j;
+#ifdef RADSORT_PHASE_PROF
+            if (tid == 0) pf[6]++;
+#endif
           }
-          gofs[tid] = segbase[(size_t)s * RADIX + tid] + (uint32_t)excl - ex;
+          st_relaxed(my, ep | ST_PREFIX | (excl + c));
         }
-        __syncthreads();
-        for (uint32_t p = tid; p < m; p += SCAT_B) {
-          const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
-          const uint32_t dg = digit_of(key_of<R, K>(x), d);
-          st_rec<R>(dst + (size_t)(gofs[dg] + p) * R, x);
-        }
+        gofs[tid] = segbase[(size_t)s * RADIX + tid] + (uint32_t)excl - ex;
+      }
+      __syncthreads();
+      RS_PROF(4);
+      for (uint32_t q = tid; q < m; q += SB) {
+        const Rec<R> x = ld_rec<R>(stage + (size_t)q * R);
+        st_rec<R>(dst + (size_t)(gofs[digit_of(key_of<R, K>(x), d)] + q) * R, x);
       }
       moved += m;
+      t = tn;
+      s = sn;
+    } else {
+      if (sg.mode == MODE_COPY) {
+        const uint8_t* src = buf_of(sg.src, recs, tmp);
+        for (uint32_t i = tid; i < m; i += SB)
+          st_rec<R>(dst + (size_t)(base + i) * R, ldg_rec<R>(src + (size_t)(base + i) * R));
+        moved += m;
+      }
+      if (tid == 0) take();
+      __syncthreads();
+      t = sh_t;
+      s = sh_s;
+      if (t < total) load(t, s);
     }
-    __syncthreads();
+    __syncthreads();  // stage / gofs / sh_* reuse
+    RS_PROF(5);
   }
   if (tid == 0 && moved) atomicAdd(&ctl->rec_scatter, moved);
+#ifdef RADSORT_PHASE_PROF
+  if (tid == 0) {
+    for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[q], pf[q]);
+  }
+#endif
+#undef RS_PROF
 }
 
 // -------------------------------------------------------------- k_children
@@ -462,7 +520,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
   __shared__ uint32_t cnt[RADIX], start[RADIX], ws[8], big[RADIX];
   __shared__ unsigned long long sna[2], so[2];
-  __shared__ uint32_t sh_d, nbig;
+  __shared__ uint32_t sh_d, nbig, nsml;
   constexpr int KW = K / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(stage + stage_bytes)[warp];
@@ -491,9 +549,18 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
   prefetch_l2(bi + gridDim.x);
   if (tid < RADIX) cnt[tid] = 0;
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-  if (tid == 0) nbig = 0;
+  if (tid == 0) { nbig = 0; nsml = 0; }
   unsigned long long done = 0;
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = 0, tB = 0;
+#define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
+#else
+#define RS_PROF(i) do { } while (0)
+#endif
   for (;;) {
+#ifdef RADSORT_PHASE_PROF
+    if (tid == 0) { tA = clock64(); pf[7]++; }
+#endif
     const uint32_t n = sg.len;
     uint8_t* out = recs + (size_t)sg.off * R;
     load(sg);
@@ -523,6 +590,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
     }
     __syncthreads();
     const uint32_t d = sh_d;
+    RS_PROF(0);
     if (d >= (uint32_t)K) {  // all keys equal: final where it is (copied out of tmp)
       if (sg.src == SRC_TMP) {
 #pragma unroll
@@ -544,6 +612,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       __syncthreads();
       const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
       if (tid < RADIX && c > es_max<R>()) big[atomicAdd(&nbig, 1u)] = tid;  // sub-bins for phase B
+      if (tid < RADIX && c > 0 && c <= es_max<R>()) atomicAdd(&nsml, 1u);  // sub-bins for phase A
       const uint32_t ex = block_excl_scan256(c, ws);
       if (tid < RADIX) start[tid] = ex;
       __syncthreads();
@@ -560,9 +629,10 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
     prefetch_l2(nb + gridDim.x);
     if (d < (uint32_t)K) {
       const uint32_t d1 = d + 1;
+      RS_PROF(1);
       // phase A, record-parallel: singletons / exhausted digits copied, sub-bins
       // of 2..ES_MAX records finished by enumeration sort
-      for (uint32_t p = tid; p < n; p += LOCAL_B) {
+      for (uint32_t p = tid; p < (nsml || d1 >= (uint32_t)K ? n : 0u); p += LOCAL_B) {
         const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
         const Key<K> kx = key_of<R, K>(x);
         const uint32_t v = digit_of(kx, d), c = cnt[v];
@@ -573,6 +643,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
           st_rec<R>(out + (size_t)(s0 + es_rank<R, K>(stage + (size_t)s0 * R, c, p - s0, kx)) * R, x);
         }
       }
+      RS_PROF(2);
       // phase B, one warp per larger sub-bin
       if (d1 < (uint32_t)K) {
         const uint32_t nb_ = nbig;
@@ -594,15 +665,23 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       }
     }
     done += n;
+    RS_PROF(3);
     __syncthreads();
+    RS_PROF(4);
     if (tid < RADIX) cnt[tid] = 0;
     if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-    if (tid == 0) nbig = 0;
+    if (tid == 0) { nbig = 0; nsml = 0; }
     if (nb >= nlist) break;
     bi = nb;
     sg = list[nb];
   }
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
+#ifdef RADSORT_PHASE_PROF
+  if (tid == 0) {
+    for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[8 + q], pf[q]);
+  }
+#endif
+#undef RS_PROF
 }
 
 }  // namespace radsort

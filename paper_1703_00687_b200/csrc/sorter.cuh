@@ -7,7 +7,6 @@ namespace radsort {
 // -------------------------------------------------------------- the sort
 template <int R, int K>
 struct Sorter {
-  static constexpr uint32_t T = tile_records<R>();
   static constexpr uint32_t C = local_capacity<R>();
   static constexpr int LOCAL_SCRATCH = (LOCAL_B / 32) * (int)sizeof(TailScratch<K>);
   static constexpr int LOCAL_DYN_MAX = LOCAL_SMEM_BYTES + LOCAL_SCRATCH;
@@ -31,7 +30,6 @@ struct Sorter {
   static void set_attrs() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(k_scatter<R, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE_BYTES);
     cudaFuncSetAttribute(k_children<R, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, CHILD_SCRATCH);
     done = true;
   }
@@ -53,9 +51,30 @@ struct Sorter {
 #undef RS_LOCAL
   }
 
+  // Scatter/histogram tile configuration: TB bytes per tile, SB threads per
+  // scatter CTA, MINB scatter CTAs per SM (RADSORT_SCATTER_CFG selects).
   static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
                             radsort_stats& stats) {
+    const char* e = getenv("RADSORT_SCATTER_CFG");
+    const int cfg = e ? atoi(e) : 0;
+    switch (cfg) {
+      case 1: return run_cfg<32768, 256, 4>(ctx, recs, tmp, n, st, stats);
+      case 2: return run_cfg<32768, 512, 2>(ctx, recs, tmp, n, st, stats);
+      case 3: return run_cfg<16384, 256, 4>(ctx, recs, tmp, n, st, stats);
+      default: return run_cfg<65536, 512, 2>(ctx, recs, tmp, n, st, stats);
+    }
+  }
+
+  template <int TB, int SB, int MINB>
+  static radsort_status run_cfg(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
+                                radsort_stats& stats) {
+    constexpr uint32_t T = (uint32_t)(TB / R);
     set_attrs();
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
+      attr = true;
+    }
     // ---- workspace
     const size_t capL = (size_t)n / C + 4;
     const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4;
@@ -85,8 +104,8 @@ struct Sorter {
     Ctl* ctl = (Ctl*)ctx->ctl.p;
 
     int occ_s = 0, occ_h = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K>, SCAT_B, TILE_BYTES);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K>, HIST_B, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB>, SB, TB);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, TB>, HIST_B, 0);
     occ_s = std::max(occ_s, 1);
     occ_h = std::max(occ_h, 1);
 
@@ -118,7 +137,7 @@ struct Sorter {
         const size_t tiles_ub = std::min(tiles_max, (size_t)n / T + n_large + 1);
         const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
         tm.begin(RADSORT_K_HIST);
-        k_hist<R, K><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
+        k_hist<R, K, TB><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
         tm.end();
         tm.begin(RADSORT_K_PLAN);
         k_plan<K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl);
@@ -129,8 +148,8 @@ struct Sorter {
         }
         const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
         tm.begin(RADSORT_K_SCATTER);
-        k_scatter<R, K><<<gs, SCAT_B, TILE_BYTES, st>>>(L[cur], tile_start, n_large, segbase, status, ctx->epoch, ctl,
-                                                        recs, tmp);
+        k_scatter<R, K, TB, SB, MINB><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status, ctx->epoch,
+                                                          ctl, recs, tmp);
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs, tmp);
@@ -170,6 +189,11 @@ struct Sorter {
     RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     RS_CUDA(cudaStreamSynchronize(st));
     const Ctl c = *ctx->h_ctl;
+#ifdef RADSORT_PHASE_PROF
+    if (log) {
+      for (int q = 0; q < 16; ++q) fprintf(stderr, "[radsort prof] %s%d %llu\n", q < 8 ? "scatter" : "local", q & 7, (unsigned long long)c.prof[q]);
+    }
+#endif
     stats.records_scattered = c.rec_scatter;
     stats.records_hist = c.rec_hist;
     stats.records_local = c.rec_local;

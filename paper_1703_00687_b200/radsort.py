@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libradsort.so")
+LIB_PATH = os.environ.get("RADSORT_LIB_PATH") or os.path.join(_HERE, "libradsort.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_NOT_INITIALIZED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_CAPACITY = range(8)
 KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "multi"]
