@@ -123,6 +123,27 @@ radsort_status radsort_sort_multi(void* dev_records, void* dev_tmp, uint64_t n_l
                                   uint64_t capacity, uint64_t* n_out, uint32_t rec_size,
                                   uint32_t key_size, void* nccl_comm, void* stream);
 
+/* In-process loopback transport for radsort_sort_multi (tests and emulation:
+ * the build pool has one GPU per box).  G host threads act as the G ranks on
+ * the current device; each calls radsort_sort_multi_loopback with its rank
+ * and its own stream and buffers.  Collectives are host barriers; the
+ * exchange is device-to-device copies.  Same algorithm as the NCCL path. */
+radsort_status radsort_loopback_create(int nranks, void** group);
+radsort_status radsort_loopback_destroy(void* group);
+radsort_status radsort_sort_multi_loopback(void* group, int rank, void* dev_records, void* dev_tmp, uint64_t n_local,
+                                           uint64_t capacity, uint64_t* n_out, uint32_t rec_size, uint32_t key_size,
+                                           void* stream);
+
+/* Host planner steps of radsort_sort_multi (pure functions; exposed so the
+ * multi-rank host logic can be tested on CPU):
+ *   quotas      q_r = floor(N/G) + (r < N mod G)                 (R11)
+ *   digit       largest v with count_lt[v] <= q (splitter refinement round)
+ *   equal split the first (Q - L) records equal to a boundary key, in
+ *               source-rank order, stay below the boundary; below[r] per rank */
+radsort_status radsort_plan_quotas(uint64_t N, int G, uint64_t* quotas);
+radsort_status radsort_plan_digit(const uint64_t* count_lt256, uint64_t q, uint32_t* digit);
+radsort_status radsort_plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, uint64_t* below);
+
 /* Splitter planning used by radsort_sort_multi (pure host function, exposed
  * for testing).  Given the GLOBAL (allreduced) 256-bin histogram `hist` of
  * the current digit over a bucket range, per-rank quotas and the global rank

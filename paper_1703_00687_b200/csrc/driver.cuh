@@ -43,7 +43,20 @@ struct Context {
   uint32_t epoch = 0;
   cudaEvent_t ev[2 * 64] = {};
   bool ev_init = false;
+  cudaEvent_t done_ev = nullptr;  // workspace free once this event (last sort's stream) completes
+  bool done_valid = false;
+  DevBuf mprobe, mlo, mhi, mlt, mle;  // multi-GPU splitter search scratch
 };
+
+// Order `st` after the previous user of the workspace (another stream may still
+// be running the tail of the last sort), and mark the end of this use.
+inline void workspace_acquire(Context* ctx, cudaStream_t st) {
+  if (ctx->done_valid) cudaStreamWaitEvent(st, ctx->done_ev, 0);
+}
+inline void workspace_release(Context* ctx, cudaStream_t st) {
+  cudaEventRecord(ctx->done_ev, st);
+  ctx->done_valid = true;
+}
 
 radsort_status ensure(DevBuf& b, size_t bytes, bool zero = false);
 
@@ -80,5 +93,33 @@ struct Timer {
 // One instantiation per built record layout (layout_R_K.cu).
 template <int R, int K>
 radsort_status run_layout(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st, radsort_stats& s);
+
+// Multi-GPU building blocks (same instantiation units).  All are synchronous
+// on `st` (they return host results) and use the context workspace.
+// multi_hist: histogram of `digit` over recs[0,n) (h256) and the AND/OR of all
+//   keys (andor4 = {~AND w0, ~AND w1, OR w0, OR w1}).
+// multi_scatter: one counting-scatter pass of recs[0,n) by `digit` into tmp;
+//   bucket b lands at [sum_{u<b} h[u], ...); h256 = multi_hist's histogram.
+// multi_bounds: for M probes, #keys < probe and <= probe in sorted [lo, hi).
+template <int R, int K>
+radsort_status multi_hist(Context* ctx, const uint8_t* recs, uint32_t n, uint32_t digit, cudaStream_t st,
+                          uint64_t* h256, uint64_t* andor4);
+template <int R, int K>
+radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, uint32_t digit, const uint64_t* h256,
+                             cudaStream_t st);
+template <int R, int K>
+radsort_status multi_bounds(Context* ctx, const uint8_t* buf, const uint32_t* lo, const uint32_t* hi,
+                            const uint64_t* probes, uint32_t M, cudaStream_t st, uint64_t* lt, uint64_t* le);
+
+struct LayoutOps {
+  radsort_status (*sort)(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
+  radsort_status (*hist)(Context*, const uint8_t*, uint32_t, uint32_t, cudaStream_t, uint64_t*, uint64_t*);
+  radsort_status (*scatter)(Context*, uint8_t*, uint8_t*, uint32_t, uint32_t, const uint64_t*, cudaStream_t);
+  radsort_status (*bounds)(Context*, const uint8_t*, const uint32_t*, const uint32_t*, const uint64_t*, uint32_t,
+                           cudaStream_t, uint64_t*, uint64_t*);
+};
+// nullptr for layouts that are not built
+const LayoutOps* layout_ops(uint32_t R, uint32_t K);
+Context* get_or_create_ctx(int device);
 
 }  // namespace radsort

@@ -1,5 +1,12 @@
-// Instantiation of the radsort level loop for rec_size=16, key_size=8.
+// Instantiation of the radsort level loop and multi-GPU building blocks for
+// rec_size=16, key_size=8.
 #include "sorter.cuh"
 namespace radsort {
 template radsort_status run_layout<16, 8>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
+template radsort_status multi_hist<16, 8>(Context*, const uint8_t*, uint32_t, uint32_t, cudaStream_t, uint64_t*,
+                                           uint64_t*);
+template radsort_status multi_scatter<16, 8>(Context*, uint8_t*, uint8_t*, uint32_t, uint32_t, const uint64_t*,
+                                              cudaStream_t);
+template radsort_status multi_bounds<16, 8>(Context*, const uint8_t*, const uint32_t*, const uint32_t*,
+                                             const uint64_t*, uint32_t, cudaStream_t, uint64_t*, uint64_t*);
 }

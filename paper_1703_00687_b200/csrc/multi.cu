@@ -1,6 +1,510 @@
-// Multi-GPU path (radsort_sort_multi): placeholder until the NCCL exchange lands.
-#include <cuda_runtime.h>
-#include "../../include/radsort.h"
-extern "C" radsort_status radsort_sort_multi(void*, void*, uint64_t, uint64_t, uint64_t*, uint32_t, uint32_t, void*, void*) {
-  return RADSORT_ERR_UNSUPPORTED;
+// radsort multi-GPU path: key-range sharding with one exchange step
+// (the paper's phase-1 "parallel processing of the whole
+// array according to the first digit", §3.1, carried across
+// GPUs).  One process (or, for tests, one host thread) per GPU rank:
+//
+//  1. agree on the layout and N = sum of n_local (allreduce min/max/sum);
+//     exact-balance quotas q_r = floor(N/G) + (r < N mod G)   (R11)
+//  2. local AND/OR of the keys -> allgather -> global first non-constant
+//     digit d0; local 256-bin histogram of d0 -> allreduce -> global H
+//  3. local counting-scatter by d0 (records -> tmp), the level-0 pass
+//  4. each boundary Q_g = q_0 + .. + q_{g-1} falls in global bucket b_g; every
+//     rank sorts its (small) bucket b_g locally, then the Q_g-th key k_g is
+//     found digit by digit: 256 probes per boundary, #keys < probe by binary
+//     search on the sorted bucket, allreduce, keep the largest digit whose
+//     count stays <= Q_g
+//  5. records equal to k_g are split across ranks by source-rank order so the
+//     quotas hold exactly (any order inside an equal-key run is correct, R2)
+//  6. send ranges are contiguous slices of tmp; counts allgathered; grouped
+//     ncclSend/ncclRecv move them into dev_records (NVLink / NVSwitch)
+//  7. the received shard is sorted by the single-GPU path.
+//
+// The algorithm is written against a small Transport interface with two
+// implementations: NCCL (the product) and an in-process loopback with host
+// threads as ranks (tests, since the pool gives one GPU per box).
+#include <nccl.h>
+
+#include <condition_variable>
+#include <numeric>
+
+#include "driver.cuh"
+
+namespace radsort {
+
+// --------------------------------------------------------------- planner
+// Pure host functions (exported for tests through the C ABI).
+static void plan_quotas(uint64_t N, int G, uint64_t* q) {
+  for (int r = 0; r < G; ++r) q[r] = N / (uint64_t)G + ((uint64_t)r < N % (uint64_t)G ? 1 : 0);
 }
+// largest digit v with count_lt[v] <= q (count_lt non-decreasing, count_lt[0] <= q)
+static uint32_t plan_digit(const uint64_t* count_lt, uint64_t q) {
+  uint32_t v = 0;
+  for (uint32_t u = 1; u < 256; ++u)
+    if (count_lt[u] <= q) v = u;
+  return v;
+}
+// records equal to the boundary key that rank r keeps below the boundary:
+// the first (Q - L) equal records in source-rank order go below.
+static void plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, uint64_t* below) {
+  uint64_t need = Q > L ? Q - L : 0;
+  for (int r = 0; r < G; ++r) {
+    const uint64_t take = std::min(need, e[r]);
+    below[r] = take;
+    need -= take;
+  }
+}
+
+// -------------------------------------------------------------- transport
+enum class ROp { Sum, Min, Max };
+
+struct Transport {
+  virtual ~Transport() {}
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  // host in -> host out (small control data)
+  virtual radsort_status allreduce(const uint64_t* in, uint64_t* out, size_t cnt, ROp op, cudaStream_t st) = 0;
+  virtual radsort_status allgather(const uint64_t* in, uint64_t* out, size_t cnt, cudaStream_t st) = 0;
+  // device data: send_bytes[p] bytes from send + send_off[p] to rank p, receive
+  // recv_bytes[p] bytes from rank p at recv + recv_off[p]
+  virtual radsort_status alltoallv(const uint8_t* send, const uint64_t* send_off, const uint64_t* send_bytes,
+                                   uint8_t* recv, const uint64_t* recv_off, const uint64_t* recv_bytes,
+                                   cudaStream_t st) = 0;
+};
+
+#define RS_NCCL(x)                                                                             \
+  do {                                                                                         \
+    ncclResult_t r_ = (x);                                                                     \
+    if (r_ != ncclSuccess) {                                                                   \
+      set_detail("%s failed: %s (%s:%d)", #x, ncclGetErrorString(r_), __FILE__, __LINE__);    \
+      return RADSORT_ERR_NCCL;                                                                 \
+    }                                                                                          \
+  } while (0)
+
+struct NcclTransport : Transport {
+  ncclComm_t comm;
+  int r = 0, g = 1;
+  DevBuf buf;
+  explicit NcclTransport(ncclComm_t c) : comm(c) {
+    ncclCommUserRank(comm, &r);
+    ncclCommCount(comm, &g);
+  }
+  ~NcclTransport() override {
+    if (buf.p) cudaFree(buf.p);
+  }
+  int rank() const override { return r; }
+  int size() const override { return g; }
+  radsort_status check(cudaStream_t st) {
+    RS_CUDA(cudaStreamSynchronize(st));
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError(comm, &ar);
+    if (ar != ncclSuccess) {
+      set_detail("NCCL async error: %s", ncclGetErrorString(ar));
+      return RADSORT_ERR_NCCL;
+    }
+    return RADSORT_OK;
+  }
+  radsort_status allreduce(const uint64_t* in, uint64_t* out, size_t cnt, ROp op, cudaStream_t st) override {
+    radsort_status rs;
+    if ((rs = ensure(buf, 2 * cnt * 8))) return rs;
+    uint64_t* d = (uint64_t*)buf.p;
+    RS_CUDA(cudaMemcpyAsync(d, in, cnt * 8, cudaMemcpyHostToDevice, st));
+    const ncclRedOp_t o = op == ROp::Sum ? ncclSum : (op == ROp::Min ? ncclMin : ncclMax);
+    RS_NCCL(ncclAllReduce(d, d + cnt, cnt, ncclUint64, o, comm, st));
+    RS_CUDA(cudaMemcpyAsync(out, d + cnt, cnt * 8, cudaMemcpyDeviceToHost, st));
+    return check(st);
+  }
+  radsort_status allgather(const uint64_t* in, uint64_t* out, size_t cnt, cudaStream_t st) override {
+    radsort_status rs;
+    if ((rs = ensure(buf, (1 + (size_t)g) * cnt * 8))) return rs;
+    uint64_t* d = (uint64_t*)buf.p;
+    RS_CUDA(cudaMemcpyAsync(d, in, cnt * 8, cudaMemcpyHostToDevice, st));
+    RS_NCCL(ncclAllGather(d, d + cnt, cnt, ncclUint64, comm, st));
+    RS_CUDA(cudaMemcpyAsync(out, d + cnt, (size_t)g * cnt * 8, cudaMemcpyDeviceToHost, st));
+    return check(st);
+  }
+  radsort_status alltoallv(const uint8_t* send, const uint64_t* send_off, const uint64_t* send_bytes, uint8_t* recv,
+                           const uint64_t* recv_off, const uint64_t* recv_bytes, cudaStream_t st) override {
+    RS_NCCL(ncclGroupStart());
+    for (int p = 0; p < g; ++p) {
+      if (send_bytes[p]) RS_NCCL(ncclSend(send + send_off[p], send_bytes[p], ncclUint8, p, comm, st));
+      if (recv_bytes[p]) RS_NCCL(ncclRecv(recv + recv_off[p], recv_bytes[p], ncclUint8, p, comm, st));
+    }
+    RS_NCCL(ncclGroupEnd());
+    return check(st);
+  }
+};
+
+// In-process loopback group: G host threads act as ranks on one device.
+struct LoopGroup {
+  int G;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<std::vector<uint64_t>> slot;
+  std::vector<const uint8_t*> sbase;
+  std::vector<std::vector<uint64_t>> soff, sbytes;
+  explicit LoopGroup(int g) : G(g), slot(g), sbase(g), soff(g), sbytes(g) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t my = gen;
+    if (++arrived == G) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my; });
+    }
+  }
+};
+
+struct LoopTransport : Transport {
+  LoopGroup* grp;
+  int r;
+  LoopTransport(LoopGroup* g, int rk) : grp(g), r(rk) {}
+  int rank() const override { return r; }
+  int size() const override { return grp->G; }
+  radsort_status allreduce(const uint64_t* in, uint64_t* out, size_t cnt, ROp op, cudaStream_t) override {
+    grp->slot[r].assign(in, in + cnt);
+    grp->barrier();
+    for (size_t i = 0; i < cnt; ++i) {
+      uint64_t a = grp->slot[0][i];
+      for (int p = 1; p < grp->G; ++p) {
+        const uint64_t b = grp->slot[p][i];
+        a = op == ROp::Sum ? a + b : (op == ROp::Min ? std::min(a, b) : std::max(a, b));
+      }
+      out[i] = a;
+    }
+    grp->barrier();
+    return RADSORT_OK;
+  }
+  radsort_status allgather(const uint64_t* in, uint64_t* out, size_t cnt, cudaStream_t) override {
+    grp->slot[r].assign(in, in + cnt);
+    grp->barrier();
+    for (int p = 0; p < grp->G; ++p) std::copy(grp->slot[p].begin(), grp->slot[p].end(), out + (size_t)p * cnt);
+    grp->barrier();
+    return RADSORT_OK;
+  }
+  radsort_status alltoallv(const uint8_t* send, const uint64_t* send_off, const uint64_t* send_bytes, uint8_t* recv,
+                           const uint64_t* recv_off, const uint64_t* recv_bytes, cudaStream_t st) override {
+    grp->sbase[r] = send;
+    grp->soff[r].assign(send_off, send_off + grp->G);
+    grp->sbytes[r].assign(send_bytes, send_bytes + grp->G);
+    RS_CUDA(cudaStreamSynchronize(st));  // every rank's send data is complete before peers read it
+    grp->barrier();
+    for (int p = 0; p < grp->G; ++p) {
+      const uint64_t b = grp->sbytes[p][r];
+      if (b != recv_bytes[p]) {
+        set_detail("loopback: rank %d expects %llu bytes from %d, sender has %llu", r,
+                   (unsigned long long)recv_bytes[p], p, (unsigned long long)b);
+        grp->barrier();
+        return RADSORT_ERR_INVALID_ARG;
+      }
+      if (b) RS_CUDA(cudaMemcpyAsync(recv + recv_off[p], grp->sbase[p] + grp->soff[p][r], b, cudaMemcpyDeviceToDevice, st));
+    }
+    RS_CUDA(cudaStreamSynchronize(st));
+    grp->barrier();
+    return RADSORT_OK;
+  }
+};
+
+// ------------------------------------------------------------- algorithm
+static void set_digit(uint64_t* key, uint32_t K, uint32_t d, uint32_t v) {
+  const uint32_t bi = K - 1 - d;
+  const uint32_t w = bi >> 3, sh = 8 * (bi & 7);
+  key[w] = (key[w] & ~(0xffull << sh)) | ((uint64_t)v << sh);
+}
+
+static radsort_status sort_multi_impl(Transport& tr, uint8_t* recs, uint8_t* tmp, uint64_t n_local, uint64_t capacity,
+                                      uint64_t* n_out, uint32_t R, uint32_t K, cudaStream_t st, radsort_stats& stats) {
+  const int G = tr.size(), me = tr.rank();
+  int dev = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  Context* ctx = get_or_create_ctx(dev);
+  if (!ctx) return RADSORT_ERR_NOT_INITIALIZED;
+  const LayoutOps* ops = layout_ops(R, K);
+  radsort_status rs;
+
+  // 1. consistent arguments (every rank fails the same way instead of hanging)
+  const uint64_t mine[5] = {R, K, ops ? 1ull : 0ull, n_local < (1ull << 32) ? 1ull : 0ull,
+                            (recs && tmp) || n_local == 0 ? 1ull : 0ull};
+  uint64_t mn[5], mx[5];
+  if ((rs = tr.allreduce(mine, mn, 5, ROp::Min, st))) return rs;
+  if ((rs = tr.allreduce(mine, mx, 5, ROp::Max, st))) return rs;
+  if (mn[0] != mx[0] || mn[1] != mx[1]) {
+    set_detail("ranks disagree on rec_size/key_size");
+    return RADSORT_ERR_INVALID_ARG;
+  }
+  if (!mn[2]) {
+    set_detail("rec_size=%u key_size=%u not built", R, K);
+    return RADSORT_ERR_UNSUPPORTED;
+  }
+  if (!mn[3] || !mn[4]) {
+    set_detail("a rank has n_local >= 2^32 or NULL buffers");
+    return RADSORT_ERR_INVALID_ARG;
+  }
+  uint64_t N = 0;
+  if ((rs = tr.allreduce(&n_local, &N, 1, ROp::Sum, st))) return rs;
+  std::vector<uint64_t> q(G), Qb(G + 1, 0);
+  plan_quotas(N, G, q.data());
+  for (int g = 0; g < G; ++g) Qb[g + 1] = Qb[g] + q[g];
+  const uint64_t cap_ok = (capacity >= q[me] && capacity >= n_local && q[me] < (1ull << 32)) ? 1 : 0;
+  uint64_t all_ok = 0;
+  if ((rs = tr.allreduce(&cap_ok, &all_ok, 1, ROp::Min, st))) return rs;
+  if (!all_ok) {
+    set_detail("capacity %llu < quota %llu or n_local on some rank", (unsigned long long)capacity,
+               (unsigned long long)q[me]);
+    return RADSORT_ERR_CAPACITY;
+  }
+  const uint32_t n = (uint32_t)n_local;
+
+  // 2. global first non-constant digit and its histogram
+  uint64_t h[256], ao[4];
+  auto hist_op = [&](uint32_t digit) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    return ops->hist(ctx, recs, n, digit, st, h, ao);
+  };
+  if ((rs = hist_op(0))) return rs;
+  std::vector<uint64_t> aog(4 * (size_t)G);
+  if ((rs = tr.allgather(ao, aog.data(), 4, st))) return rs;
+  uint64_t AND[2] = {~0ull, ~0ull}, OR[2] = {0, 0};
+  for (int p = 0; p < G; ++p)
+    for (int w = 0; w < 2; ++w) {
+      AND[w] &= ~aog[4 * p + w];
+      OR[w] |= aog[4 * p + 2 + w];
+    }
+  uint32_t d0 = 0;
+  for (; d0 < K; ++d0) {
+    const uint32_t bi = K - 1 - d0;
+    if (((AND[bi >> 3] ^ OR[bi >> 3]) >> (8 * (bi & 7))) & 255) break;
+  }
+  if (d0 >= K) d0 = 0;  // every key equal: one bucket, split by quotas
+  if (d0 != 0 && (rs = hist_op(d0))) return rs;
+  uint64_t H[256];
+  if ((rs = tr.allreduce(h, H, 256, ROp::Sum, st))) return rs;
+  stats.first_digit = d0;
+
+  // 3. level-0 pass: records -> tmp grouped by d0
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if ((rs = ops->scatter(ctx, recs, tmp, n, d0, h, st))) return rs;
+  }
+  uint64_t lbase[257];
+  lbase[0] = 0;
+  for (int b = 0; b < 256; ++b) lbase[b + 1] = lbase[b] + h[b];
+  uint64_t Hbase[257];
+  Hbase[0] = 0;
+  for (int b = 0; b < 256; ++b) Hbase[b + 1] = Hbase[b] + H[b];
+
+  // 4. boundaries: bucket, local sort of each distinct straddling bucket
+  const int NB = G - 1;
+  std::vector<uint32_t> bk(NB, 0);
+  std::vector<char> active(NB, 0);
+  for (int g = 1; g < G; ++g) {
+    const uint64_t Qg = Qb[g];
+    if (Qg >= N) continue;
+    uint32_t b = 0;
+    while (Qg >= Hbase[b + 1]) ++b;
+    bk[g - 1] = b;
+    active[g - 1] = 1;
+  }
+  {
+    std::vector<uint32_t> done;
+    for (int i = 0; i < NB; ++i) {
+      if (!active[i] || std::find(done.begin(), done.end(), bk[i]) != done.end()) continue;
+      done.push_back(bk[i]);
+      const uint64_t off = lbase[bk[i]], len = h[bk[i]];
+      if (len > 1) {
+        radsort_stats sub = {};
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((rs = ops->sort(ctx, tmp + off * R, recs + off * R, (uint32_t)len, st, sub))) return rs;
+      }
+    }
+    RS_CUDA(cudaStreamSynchronize(st));
+  }
+  // digit-by-digit selection of the boundary keys k_g
+  std::vector<uint64_t> key(2 * (size_t)NB, 0);
+  for (int i = 0; i < NB; ++i) {
+    key[2 * i] = AND[0];  // digits constant over all keys are fixed by the global AND (== OR there)
+    key[2 * i + 1] = K == 16 ? AND[1] : 0;
+    if (active[i]) set_digit(&key[2 * i], K, d0, bk[i]);
+  }
+  std::vector<uint32_t> lo(256 * (size_t)NB), hi(256 * (size_t)NB);
+  std::vector<uint64_t> probes(512 * (size_t)NB), lt(256 * (size_t)NB), le(256 * (size_t)NB), glt(256 * (size_t)NB);
+  for (int i = 0; i < NB; ++i)
+    for (int v = 0; v < 256; ++v) {
+      lo[256 * i + v] = (uint32_t)lbase[bk[i]];
+      hi[256 * i + v] = (uint32_t)(lbase[bk[i]] + (active[i] ? h[bk[i]] : 0));
+    }
+  for (uint32_t d = d0 + 1; d < K && NB > 0; ++d) {
+    const uint32_t bi = K - 1 - d;
+    if (!(((AND[bi >> 3] ^ OR[bi >> 3]) >> (8 * (bi & 7))) & 255)) continue;  // globally constant digit
+    for (int i = 0; i < NB; ++i)
+      for (uint32_t v = 0; v < 256; ++v) {
+        uint64_t* pk = &probes[2 * (256 * (size_t)i + v)];
+        pk[0] = key[2 * i];
+        pk[1] = key[2 * i + 1];
+        set_digit(pk, K, d, v);
+        for (uint32_t dd = d + 1; dd < K; ++dd) set_digit(pk, K, dd, 0);
+      }
+    {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      if ((rs = ops->bounds(ctx, tmp, lo.data(), hi.data(), probes.data(), 256 * NB, st, lt.data(), le.data())))
+        return rs;
+    }
+    if ((rs = tr.allreduce(lt.data(), glt.data(), 256 * (size_t)NB, ROp::Sum, st))) return rs;
+    for (int i = 0; i < NB; ++i) {
+      if (!active[i]) continue;
+      const uint64_t target = Qb[i + 1] - Hbase[bk[i]];  // position of k_g inside bucket b_g
+      set_digit(&key[2 * i], K, d, plan_digit(&glt[256 * (size_t)i], target));
+    }
+  }
+  // 5. exact cut points: keys < k_g, then the equal run split by source rank
+  for (int i = 0; i < NB; ++i) {
+    probes[2 * i] = key[2 * i];
+    probes[2 * i + 1] = key[2 * i + 1];
+    lo[i] = (uint32_t)lbase[bk[i]];
+    hi[i] = (uint32_t)(lbase[bk[i]] + (active[i] ? h[bk[i]] : 0));
+  }
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if ((rs = ops->bounds(ctx, tmp, lo.data(), hi.data(), probes.data(), NB, st, lt.data(), le.data()))) return rs;
+  }
+  std::vector<uint64_t> mine2(2 * (size_t)NB), all2(2 * (size_t)NB * G);
+  for (int i = 0; i < NB; ++i) {
+    mine2[2 * i] = lt[i];
+    mine2[2 * i + 1] = le[i] - lt[i];
+  }
+  if (NB > 0 && (rs = tr.allgather(mine2.data(), all2.data(), 2 * (size_t)NB, st))) return rs;
+  std::vector<uint64_t> cut(G + 1, 0);
+  cut[G] = n_local;
+  for (int g = 1; g < G; ++g) {
+    const int i = g - 1;
+    if (!active[i]) {
+      cut[g] = n_local;
+      continue;
+    }
+    uint64_t L = Hbase[bk[i]];
+    std::vector<uint64_t> e(G), below(G);
+    for (int p = 0; p < G; ++p) {
+      L += all2[(size_t)p * 2 * NB + 2 * i];
+      e[p] = all2[(size_t)p * 2 * NB + 2 * i + 1];
+    }
+    plan_equal_split(e.data(), G, L, Qb[g], below.data());
+    cut[g] = lbase[bk[i]] + lt[i] + below[me];
+  }
+  for (int g = 1; g <= G; ++g) cut[g] = std::max(cut[g], cut[g - 1]);
+
+  // 6. exchange
+  std::vector<uint64_t> sc(G), S((size_t)G * G);
+  for (int g = 0; g < G; ++g) sc[g] = cut[g + 1] - cut[g];
+  if ((rs = tr.allgather(sc.data(), S.data(), G, st))) return rs;
+  std::vector<uint64_t> soff(G), sbytes(G), roff(G), rbytes(G);
+  uint64_t got = 0;
+  for (int p = 0; p < G; ++p) {
+    soff[p] = cut[p] * R;
+    sbytes[p] = sc[p] * R;
+    roff[p] = got * R;
+    rbytes[p] = S[(size_t)p * G + me] * R;
+    got += S[(size_t)p * G + me];
+  }
+  if (got != q[me]) {
+    set_detail("exchange plan gives %llu records, quota %llu", (unsigned long long)got, (unsigned long long)q[me]);
+    return RADSORT_ERR_CUDA;
+  }
+  if ((rs = tr.alltoallv(tmp, soff.data(), sbytes.data(), recs, roff.data(), rbytes.data(), st))) return rs;
+  stats.nvlink_bytes_sent = (n_local - sc[me]) * R;
+  stats.nvlink_bytes_recv = (got - S[(size_t)me * G + me]) * R;
+
+  // 7. local sort of the received key range
+  radsort_stats sub = {};
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if ((rs = ops->sort(ctx, recs, tmp, (uint32_t)got, st, sub))) return rs;
+  }
+  stats.levels = sub.levels;
+  stats.scatter_passes = sub.scatter_passes + 1;
+  stats.records_scattered = sub.records_scattered + n_local;
+  stats.records_hist = sub.records_hist + n_local;
+  stats.records_local = sub.records_local;
+  stats.records_tiny = sub.records_tiny;
+  for (int k = 0; k < RADSORT_K_COUNT; ++k) {
+    stats.kernel_launches[k] += sub.kernel_launches[k];
+    stats.kernel_ms[k] += sub.kernel_ms[k];
+    stats.kernel_bytes[k] += sub.kernel_bytes[k];
+  }
+  stats.n = got;
+  *n_out = got;
+  return RADSORT_OK;
+}
+
+void set_last_stats(const radsort_stats& s);
+
+}  // namespace radsort
+
+using namespace radsort;
+
+extern "C" {
+
+radsort_status radsort_sort_multi(void* dev_records, void* dev_tmp, uint64_t n_local, uint64_t capacity,
+                                  uint64_t* n_out, uint32_t rec_size, uint32_t key_size, void* nccl_comm,
+                                  void* stream) {
+  if (!nccl_comm || !n_out) {
+    set_detail("NULL nccl_comm or n_out");
+    return RADSORT_ERR_INVALID_ARG;
+  }
+  NcclTransport tr((ncclComm_t)nccl_comm);
+  radsort_stats s = {};
+  s.rec_size = rec_size;
+  s.key_size = key_size;
+  const radsort_status rs = sort_multi_impl(tr, (uint8_t*)dev_records, (uint8_t*)dev_tmp, n_local, capacity, n_out,
+                                            rec_size, key_size, (cudaStream_t)stream, s);
+  set_last_stats(s);
+  return rs;
+}
+
+radsort_status radsort_loopback_create(int nranks, void** group) {
+  if (nranks < 1 || !group) return RADSORT_ERR_INVALID_ARG;
+  *group = new LoopGroup(nranks);
+  return RADSORT_OK;
+}
+
+radsort_status radsort_loopback_destroy(void* group) {
+  delete static_cast<LoopGroup*>(group);
+  return RADSORT_OK;
+}
+
+radsort_status radsort_sort_multi_loopback(void* group, int rank, void* dev_records, void* dev_tmp, uint64_t n_local,
+                                           uint64_t capacity, uint64_t* n_out, uint32_t rec_size, uint32_t key_size,
+                                           void* stream) {
+  LoopGroup* g = static_cast<LoopGroup*>(group);
+  if (!g || rank < 0 || rank >= g->G || !n_out) return RADSORT_ERR_INVALID_ARG;
+  LoopTransport tr(g, rank);
+  radsort_stats s = {};
+  s.rec_size = rec_size;
+  s.key_size = key_size;
+  const radsort_status rs = sort_multi_impl(tr, (uint8_t*)dev_records, (uint8_t*)dev_tmp, n_local, capacity, n_out,
+                                            rec_size, key_size, (cudaStream_t)stream, s);
+  set_last_stats(s);
+  return rs;
+}
+
+radsort_status radsort_plan_quotas(uint64_t N, int G, uint64_t* quotas) {
+  if (G < 1 || !quotas) return RADSORT_ERR_INVALID_ARG;
+  plan_quotas(N, G, quotas);
+  return RADSORT_OK;
+}
+
+radsort_status radsort_plan_digit(const uint64_t* count_lt256, uint64_t q, uint32_t* digit) {
+  if (!count_lt256 || !digit || count_lt256[0] > q) return RADSORT_ERR_INVALID_ARG;
+  *digit = plan_digit(count_lt256, q);
+  return RADSORT_OK;
+}
+
+radsort_status radsort_plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, uint64_t* below) {
+  if (!e || !below || G < 1) return RADSORT_ERR_INVALID_ARG;
+  plan_equal_split(e, G, L, Q, below);
+  return RADSORT_OK;
+}
+
+}  // extern "C"

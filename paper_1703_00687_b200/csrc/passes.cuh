@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
 template <int K>
 __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __restrict__ hist,
                                                 const unsigned long long* __restrict__ andor,
-                                                uint32_t* __restrict__ segbase, Seg* large_next, Ctl* ctl) {
+                                                uint32_t* __restrict__ segbase, Seg* large_next, Ctl* ctl,
+                                                int force = 0) {
   __shared__ uint32_t ws[8];
   __shared__ int sh_const;
   const uint32_t s = blockIdx.x;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __res
   if (tid == 0) sh_const = 0;
   __syncthreads();
   const uint32_t c = hist[(size_t)s * RADIX + tid];
-  if (c == sg.len) sh_const = 1;
+  if (c == sg.len && !force) sh_const = 1;
   __syncthreads();
   if (sh_const) {
     if (tid == 0) {
@@ -682,6 +683,34 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
   }
 #endif
 #undef RS_PROF
+}
+
+// -------------------------------------------------------------- k_bounds
+// Multi-GPU splitter search: for probe m, the number of keys < probe (lt) and
+// <= probe (le) inside the SORTED record range [lo[m], hi[m]) of buf (binary
+// search; the keys there are sorted by the single-GPU path first).
+template <int R, int K>
+__global__ void k_bounds(const uint8_t* __restrict__ buf, const uint32_t* __restrict__ lo,
+                         const uint32_t* __restrict__ hi, const unsigned long long* __restrict__ probes, uint32_t M,
+                         unsigned long long* __restrict__ lt, unsigned long long* __restrict__ le) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  Key<K> x;
+  x.w0 = probes[(size_t)m * 2];
+  if constexpr (K == 16) x.w1 = probes[(size_t)m * 2 + 1];
+  uint32_t a = lo[m], b = hi[m];
+  while (a < b) {  // first key >= x
+    const uint32_t mid = a + ((b - a) >> 1);
+    if (key_lt(ld_key<R, K>(buf + (size_t)mid * R), x)) a = mid + 1; else b = mid;
+  }
+  const uint32_t l = a;
+  b = hi[m];
+  while (a < b) {  // first key > x
+    const uint32_t mid = a + ((b - a) >> 1);
+    if (!key_lt(x, ld_key<R, K>(buf + (size_t)mid * R))) a = mid + 1; else b = mid;
+  }
+  lt[m] = l - lo[m];
+  le[m] = a - lo[m];
 }
 
 }  // namespace radsort

@@ -19,6 +19,8 @@ void set_detail(const char* fmt, ...) {
   g_detail = b;
 }
 
+void set_last_stats(const radsort_stats& s) { g_stats = s; }
+
 static std::mutex g_ctx_mu;
 static std::vector<Context*> g_ctx;
 
@@ -26,6 +28,29 @@ static Context* get_ctx(int dev) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
   for (auto* c : g_ctx)
     if (c->device == dev) return c;
+  return nullptr;
+}
+
+Context* get_or_create_ctx(int dev) {
+  Context* c = get_ctx(dev);
+  if (!c && radsort_init(dev) == RADSORT_OK) c = get_ctx(dev);
+  return c;
+}
+
+const LayoutOps* layout_ops(uint32_t R, uint32_t K) {
+#define RS_OPS(r, k) \
+  static const LayoutOps ops_##r##_##k = {run_layout<r, k>, multi_hist<r, k>, multi_scatter<r, k>, multi_bounds<r, k>}
+  RS_OPS(8, 8);
+  RS_OPS(16, 8);
+  RS_OPS(16, 16);
+  RS_OPS(32, 8);
+  RS_OPS(32, 16);
+#undef RS_OPS
+  if (R == 8 && K == 8) return &ops_8_8;
+  if (R == 16 && K == 8) return &ops_16_8;
+  if (R == 16 && K == 16) return &ops_16_16;
+  if (R == 32 && K == 8) return &ops_32_8;
+  if (R == 32 && K == 16) return &ops_32_16;
   return nullptr;
 }
 
@@ -97,6 +122,7 @@ radsort_status radsort_init(int device) {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   for (auto& ev : c->ev) cudaEventCreate(&ev);
+  cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming);
   cudaSetDevice(prev);
   c->ev_init = true;
   g_ctx.push_back(c);
@@ -228,13 +254,15 @@ void radsort_finalize(void) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->large[0], &c->large[1], &c->local[0], &c->local[1], &c->hist, &c->andor, &c->segbase,
-                      &c->tile_start, &c->status, &c->ctl, &c->host_io[0], &c->host_io[1]};
+    DevBuf* bufs[] = {&c->large[0], &c->large[1], &c->local[0], &c->local[1], &c->hist,     &c->andor,
+                      &c->segbase,  &c->tile_start, &c->status, &c->ctl,   &c->host_io[0], &c->host_io[1],
+                      &c->mprobe,   &c->mlo,      &c->mhi,      &c->mlt,   &c->mle};
     for (auto* b : bufs)
       if (b->p) cudaFree(b->p);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     for (auto& ev : c->ev)
       if (ev) cudaEventDestroy(ev);
+    if (c->done_ev) cudaEventDestroy(c->done_ev);
     cudaSetDevice(prev);
     delete c;
   }

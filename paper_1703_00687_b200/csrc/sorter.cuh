@@ -51,6 +51,48 @@ struct Sorter {
 #undef RS_LOCAL
   }
 
+  struct Views {
+    Seg* L[2];
+    Seg* Lo[2];
+    uint32_t *hist, *segbase, *tile_start;
+    unsigned long long *andor, *status;
+    Ctl* ctl;
+    size_t tiles_max;
+  };
+
+  // Grow the workspace for n records and tiles of T records.
+  static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v) {
+    const size_t capL = (size_t)n / C + 4;
+    const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4;
+    const size_t tiles_max = (size_t)n / T + capL + 4;
+    radsort_status rs;
+    if ((rs = ensure(ctx->large[0], capL * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->large[1], capL * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->local[0], capLoc * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->local[1], capLoc * sizeof(Seg)))) return rs;
+    if ((rs = ensure(ctx->hist, capL * RADIX * sizeof(uint32_t)))) return rs;
+    if ((rs = ensure(ctx->segbase, capL * RADIX * sizeof(uint32_t)))) return rs;
+    if ((rs = ensure(ctx->andor, capL * 4 * sizeof(unsigned long long)))) return rs;
+    if ((rs = ensure(ctx->tile_start, (capL + 1) * sizeof(uint32_t)))) return rs;
+    const size_t old_status = ctx->status.bytes;
+    if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
+    if (ctx->status.bytes != old_status) ctx->epoch = 0;
+    if ((rs = ensure(ctx->ctl, sizeof(Ctl)))) return rs;
+    if (!ctx->h_ctl) RS_CUDA(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
+    v.L[0] = (Seg*)ctx->large[0].p;
+    v.L[1] = (Seg*)ctx->large[1].p;
+    v.Lo[0] = (Seg*)ctx->local[0].p;
+    v.Lo[1] = (Seg*)ctx->local[1].p;
+    v.hist = (uint32_t*)ctx->hist.p;
+    v.segbase = (uint32_t*)ctx->segbase.p;
+    v.andor = (unsigned long long*)ctx->andor.p;
+    v.tile_start = (uint32_t*)ctx->tile_start.p;
+    v.status = (unsigned long long*)ctx->status.p;
+    v.ctl = (Ctl*)ctx->ctl.p;
+    v.tiles_max = tiles_max;
+    return RADSORT_OK;
+  }
+
   // Scatter/histogram tile configuration: TB bytes per tile, SB threads per
   // scatter CTA, MINB scatter CTAs per SM (RADSORT_SCATTER_CFG selects).
   static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
@@ -75,33 +117,18 @@ struct Sorter {
       cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
       attr = true;
     }
-    // ---- workspace
-    const size_t capL = (size_t)n / C + 4;
-    const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4;
-    const size_t tiles_max = (size_t)n / T + capL + 4;
-    radsort_status rs;
-    if ((rs = ensure(ctx->large[0], capL * sizeof(Seg)))) return rs;
-    if ((rs = ensure(ctx->large[1], capL * sizeof(Seg)))) return rs;
-    if ((rs = ensure(ctx->local[0], capLoc * sizeof(Seg)))) return rs;
-    if ((rs = ensure(ctx->local[1], capLoc * sizeof(Seg)))) return rs;
-    if ((rs = ensure(ctx->hist, capL * RADIX * sizeof(uint32_t)))) return rs;
-    if ((rs = ensure(ctx->segbase, capL * RADIX * sizeof(uint32_t)))) return rs;
-    if ((rs = ensure(ctx->andor, capL * 4 * sizeof(unsigned long long)))) return rs;
-    if ((rs = ensure(ctx->tile_start, (capL + 1) * sizeof(uint32_t)))) return rs;
-    const size_t old_status = ctx->status.bytes;
-    if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
-    if (ctx->status.bytes != old_status) ctx->epoch = 0;
-    if ((rs = ensure(ctx->ctl, sizeof(Ctl)))) return rs;
-    if (!ctx->h_ctl) RS_CUDA(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
-
-    Seg* L[2] = {(Seg*)ctx->large[0].p, (Seg*)ctx->large[1].p};
-    Seg* Lo[2] = {(Seg*)ctx->local[0].p, (Seg*)ctx->local[1].p};
-    uint32_t* hist = (uint32_t*)ctx->hist.p;
-    uint32_t* segbase = (uint32_t*)ctx->segbase.p;
-    unsigned long long* andor = (unsigned long long*)ctx->andor.p;
-    uint32_t* tile_start = (uint32_t*)ctx->tile_start.p;
-    unsigned long long* status = (unsigned long long*)ctx->status.p;
-    Ctl* ctl = (Ctl*)ctx->ctl.p;
+    Views v;
+    radsort_status rs = prepare(ctx, n, T, v);
+    if (rs) return rs;
+    Seg** L = v.L;
+    Seg** Lo = v.Lo;
+    uint32_t* hist = v.hist;
+    uint32_t* segbase = v.segbase;
+    unsigned long long* andor = v.andor;
+    uint32_t* tile_start = v.tile_start;
+    unsigned long long* status = v.status;
+    Ctl* ctl = v.ctl;
+    const size_t tiles_max = v.tiles_max;
 
     int occ_s = 0, occ_h = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB>, SB, TB);
@@ -214,7 +241,105 @@ struct Sorter {
 
 template <int R, int K>
 radsort_status run_layout(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st, radsort_stats& s) {
-  return Sorter<R, K>::run(ctx, recs, tmp, n, st, s);
+  workspace_acquire(ctx, st);
+  const radsort_status rs = Sorter<R, K>::run(ctx, recs, tmp, n, st, s);
+  workspace_release(ctx, st);
+  return rs;
+}
+
+// ------------------------------------------------ multi-GPU building blocks
+constexpr int MULTI_TB = 65536, MULTI_SB = 512, MULTI_MINB = 2;
+
+template <int R, int K>
+radsort_status multi_hist(Context* ctx, const uint8_t* recs, uint32_t n, uint32_t digit, cudaStream_t st,
+                          uint64_t* h256, uint64_t* andor4) {
+  using S = Sorter<R, K>;
+  constexpr uint32_t T = MULTI_TB / R;
+  workspace_acquire(ctx, st);
+  typename S::Views v;
+  radsort_status rs = S::prepare(ctx, n > 0 ? n : 1, T, v);
+  if (rs) return rs;
+  const Seg sg = {0u, n, (uint8_t)digit, SRC_REC, MODE_NONE, 0, 0};
+  RS_CUDA(cudaMemcpyAsync(v.L[0], &sg, sizeof(Seg), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemsetAsync(v.hist, 0, RADIX * sizeof(uint32_t), st));
+  RS_CUDA(cudaMemsetAsync(v.andor, 0, 4 * sizeof(unsigned long long), st));
+  RS_CUDA(cudaMemsetAsync(v.ctl, 0, sizeof(Ctl), st));
+  k_prep<<<1, 1024, 0, st>>>(v.L[0], 1, T, v.tile_start, v.ctl, 1);
+  int occ_h = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, MULTI_TB>, HIST_B, 0);
+  const unsigned gh = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_h));
+  k_hist<R, K, MULTI_TB><<<gh, HIST_B, 0, st>>>(v.L[0], v.tile_start, 1, v.ctl, v.hist, v.andor, (const uint8_t*)recs,
+                                                 (const uint8_t*)recs);
+  uint32_t h32[RADIX];
+  RS_CUDA(cudaMemcpyAsync(h32, v.hist, sizeof h32, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaMemcpyAsync(andor4, v.andor, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < RADIX; ++b) h256[b] = h32[b];
+  workspace_release(ctx, st);
+  return RADSORT_OK;
+}
+
+template <int R, int K>
+radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, uint32_t digit, const uint64_t* h256,
+                             cudaStream_t st) {
+  using S = Sorter<R, K>;
+  constexpr uint32_t T = MULTI_TB / R;
+  if (n == 0) return RADSORT_OK;
+  workspace_acquire(ctx, st);
+  typename S::Views v;
+  radsort_status rs = S::prepare(ctx, n, T, v);
+  if (rs) return rs;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         MULTI_TB);
+    attr = true;
+  }
+  const Seg sg = {0u, n, (uint8_t)digit, SRC_REC, MODE_NONE, 0, 0};
+  uint32_t h32[RADIX];
+  for (int b = 0; b < RADIX; ++b) h32[b] = (uint32_t)h256[b];
+  RS_CUDA(cudaMemcpyAsync(v.L[0], &sg, sizeof(Seg), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(v.hist, h32, sizeof h32, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemsetAsync(v.ctl, 0, sizeof(Ctl), st));
+  k_prep<<<1, 1024, 0, st>>>(v.L[0], 1, T, v.tile_start, v.ctl, 1);
+  k_plan<K><<<1, RADIX, 0, st>>>(v.L[0], v.hist, v.andor, v.segbase, v.L[1], v.ctl, 1);
+  if (++ctx->epoch >= 65536) {
+    RS_CUDA(cudaMemsetAsync(v.status, 0, ctx->status.bytes, st));
+    ctx->epoch = 1;
+  }
+  int occ_s = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB>, MULTI_SB,
+                                                MULTI_TB);
+  const unsigned gs = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_s));
+  k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB><<<gs, MULTI_SB, MULTI_TB, st>>>(
+      v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp);
+  RS_CUDA(cudaGetLastError());
+  RS_CUDA(cudaStreamSynchronize(st));
+  workspace_release(ctx, st);
+  return RADSORT_OK;
+}
+
+template <int R, int K>
+radsort_status multi_bounds(Context* ctx, const uint8_t* buf, const uint32_t* lo, const uint32_t* hi,
+                            const uint64_t* probes, uint32_t M, cudaStream_t st, uint64_t* lt, uint64_t* le) {
+  if (M == 0) return RADSORT_OK;
+  radsort_status rs;
+  if ((rs = ensure(ctx->mprobe, (size_t)M * 16))) return rs;
+  if ((rs = ensure(ctx->mlo, (size_t)M * 4))) return rs;
+  if ((rs = ensure(ctx->mhi, (size_t)M * 4))) return rs;
+  if ((rs = ensure(ctx->mlt, (size_t)M * 8))) return rs;
+  if ((rs = ensure(ctx->mle, (size_t)M * 8))) return rs;
+  RS_CUDA(cudaMemcpyAsync(ctx->mprobe.p, probes, (size_t)M * 16, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(ctx->mlo.p, lo, (size_t)M * 4, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(ctx->mhi.p, hi, (size_t)M * 4, cudaMemcpyHostToDevice, st));
+  k_bounds<R, K><<<(M + 255) / 256, 256, 0, st>>>(buf, (const uint32_t*)ctx->mlo.p, (const uint32_t*)ctx->mhi.p,
+                                                  (const unsigned long long*)ctx->mprobe.p, M,
+                                                  (unsigned long long*)ctx->mlt.p, (unsigned long long*)ctx->mle.p);
+  RS_CUDA(cudaGetLastError());
+  RS_CUDA(cudaMemcpyAsync(lt, ctx->mlt.p, (size_t)M * 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaMemcpyAsync(le, ctx->mle.p, (size_t)M * 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  return RADSORT_OK;
 }
 
 }  // namespace radsort

@@ -19,7 +19,8 @@ KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "mul
 # every symbol include/radsort.h declares
 EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
            "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
-           "radsort_version"]
+           "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
+           "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split"]
 
 
 class Stats(ctypes.Structure):
@@ -62,8 +63,15 @@ def _load():
     L.radsort_finalize.argtypes = []
     L.radsort_finalize.restype = None
     L.radsort_version.restype = ctypes.c_char_p
+    L.radsort_loopback_create.argtypes = [i32, ctypes.POINTER(vp)]
+    L.radsort_loopback_destroy.argtypes = [vp]
+    L.radsort_sort_multi_loopback.argtypes = [vp, i32, vp, vp, u64, u64, ctypes.POINTER(u64), u32, u32, vp]
+    L.radsort_plan_quotas.argtypes = [u64, i32, vp]
+    L.radsort_plan_digit.argtypes = [vp, u64, ctypes.POINTER(u32)]
+    L.radsort_plan_equal_split.argtypes = [vp, i32, u64, u64, vp]
     for f in ("radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
-              "radsort_set_timing", "radsort_last_stats"):
+              "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
+              "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split"):
         getattr(L, f).restype = i32
     return L
 
@@ -139,6 +147,56 @@ def sort_multi(records, tmp, n_local: int, key_size: int, group=None, stream=Non
     _check(lib.radsort_sort_multi(ctypes.c_void_p(records.data_ptr()), ctypes.c_void_p(tmp.data_ptr()), n_local, cap,
                                   ctypes.byref(n_out), R, key_size, ctypes.c_void_p(comm), _stream_ptr(stream)))
     return int(n_out.value)
+
+
+class LoopbackGroup:
+    """G in-process ranks on one GPU (host threads), same algorithm as NCCL."""
+
+    def __init__(self, nranks: int):
+        self.handle = ctypes.c_void_p()
+        _check(lib.radsort_loopback_create(nranks, ctypes.byref(self.handle)))
+        self.nranks = nranks
+
+    def sort(self, rank: int, records, tmp, n_local: int, key_size: int, stream=None) -> int:
+        R = records.shape[1]
+        cap = min(records.shape[0], tmp.numel() * tmp.element_size() // R)
+        n_out = ctypes.c_uint64(0)
+        _check(lib.radsort_sort_multi_loopback(self.handle, rank, ctypes.c_void_p(records.data_ptr()),
+                                               ctypes.c_void_p(tmp.data_ptr()), n_local, cap, ctypes.byref(n_out), R,
+                                               key_size, _stream_ptr(stream)))
+        return int(n_out.value)
+
+    def close(self):
+        if self.handle:
+            lib.radsort_loopback_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+
+def plan_quotas(N: int, G: int):
+    import numpy as np
+
+    q = np.zeros(G, dtype=np.uint64)
+    _check(lib.radsort_plan_quotas(N, G, ctypes.c_void_p(q.ctypes.data)))
+    return q
+
+
+def plan_digit(count_lt256, q: int) -> int:
+    import numpy as np
+
+    c = np.ascontiguousarray(count_lt256, dtype=np.uint64)
+    d = ctypes.c_uint32(0)
+    _check(lib.radsort_plan_digit(ctypes.c_void_p(c.ctypes.data), q, ctypes.byref(d)))
+    return int(d.value)
+
+
+def plan_equal_split(e, L: int, Q: int):
+    import numpy as np
+
+    e = np.ascontiguousarray(e, dtype=np.uint64)
+    below = np.zeros_like(e)
+    _check(lib.radsort_plan_equal_split(ctypes.c_void_p(e.ctypes.data), len(e), L, Q,
+                                        ctypes.c_void_p(below.ctypes.data)))
+    return below
 
 
 def locate_bucket(hist256, q: int):
