@@ -199,6 +199,141 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
   if (tid == 0 && cnt_recs) atomicAdd((unsigned long long*)&ctl->rec_hist, cnt_recs);
 }
 
+// -------------------------------------------------------------- k_hist_pre
+// k_hist plus the cross-tile prefix the scatter needs, so the scatter has no
+// inter-CTA dependency (reduce-then-scan instead of look-back).  CTA c owns the
+// contiguous chunk of tiles [c*per, (c+1)*per).  For every tile it writes
+// tile_pre[t][v] = count of digit v in the tiles of the same segment that
+// precede t inside the chunk; per chunk it writes its first and last segment
+// and ch_tot[c][v] = count of digit v of the chunk's last segment in the chunk
+// (k_carry turns these into each chunk's carry-in).
+constexpr uint32_t NO_SEG = 0xffffffffu;
+template <int R, int K, int TB>
+__global__ void __launch_bounds__(HIST_B) k_hist_pre(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
+                                                     uint32_t nseg, const Ctl* __restrict__ ctl,
+                                                     uint32_t* __restrict__ hist, unsigned long long* __restrict__ andor,
+                                                     const uint8_t* recs, const uint8_t* tmp, uint32_t* __restrict__ tile_pre,
+                                                     uint32_t* __restrict__ ch_first, uint32_t* __restrict__ ch_last,
+                                                     uint32_t* __restrict__ ch_tot) {
+  constexpr uint32_t T = (uint32_t)(TB / R);
+  constexpr int KW = K / 8;
+  constexpr int U = R <= 8 ? 16 : 8;  // keys in flight per thread
+  __shared__ uint32_t h[RADIX], run[RADIX];
+  __shared__ unsigned long long sna[2], so[2];
+  const uint32_t total = ctl->tiles_total;
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t c = blockIdx.x;
+  const uint32_t t0 = c * per, t1 = min(total, t0 + per);
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (t0 >= t1) {
+    if (tid == 0) ch_first[c] = ch_last[c] = NO_SEG;
+    return;
+  }
+  for (int i = tid; i < RADIX; i += HIST_B) h[i] = run[i] = 0;
+  if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+  __syncthreads();
+  uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+  unsigned long long cnt_recs = 0;
+  uint32_t cur = seg_of_tile(tile_start, nseg, t0);
+  uint32_t cur_end = tile_start[cur + 1];
+  if (tid == 0) ch_first[c] = cur;
+  auto flush = [&](uint32_t s) {
+#pragma unroll
+    for (int w = 0; w < KW; ++w) {
+      const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+      const uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+      const uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+      const uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+      if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
+      na[w] = 0;
+      o[w] = 0;
+    }
+    __syncthreads();
+    for (int i = tid; i < RADIX; i += HIST_B) {
+      if (run[i]) atomicAdd(&hist[(size_t)s * RADIX + i], run[i]);
+      run[i] = 0;
+    }
+    if (tid < KW) {
+      if (sna[tid]) atomicOr(&andor[(size_t)s * 4 + tid], sna[tid]);
+      if (so[tid]) atomicOr(&andor[(size_t)s * 4 + 2 + tid], so[tid]);
+    }
+    __syncthreads();
+    if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+  };
+  for (uint32_t t = t0; t < t1; ++t) {
+    if (t >= cur_end) {
+      flush(cur);
+      cur = seg_of_tile(tile_start, nseg, t);
+      cur_end = tile_start[cur + 1];
+    }
+    const Seg sg = segs[cur];
+    if (sg.flags & FLAG_EQUAL) continue;
+    const uint32_t lt = t - tile_start[cur];
+    const uint32_t m = min(T, sg.len - lt * T);
+    const uint8_t* src = (sg.src == SRC_TMP ? tmp : recs) + (size_t)(sg.off + lt * T) * R;
+    const uint32_t d = sg.depth;
+    for (uint32_t i0 = tid; i0 < m; i0 += HIST_B * U) {
+      Key<K> k[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + u * HIST_B;
+        if (i < m) k[u] = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + u * HIST_B;
+        if (i < m) {
+          atomicAdd(&h[digit_of(k[u], d)], 1u);
+          na[0] |= ~k[u].w0; o[0] |= k[u].w0;
+          if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < RADIX; i += HIST_B) {
+      tile_pre[(size_t)t * RADIX + i] = run[i];
+      run[i] += h[i];
+      h[i] = 0;
+    }
+    __syncthreads();
+    cnt_recs += m;
+  }
+  for (int i = tid; i < RADIX; i += HIST_B) ch_tot[(size_t)c * RADIX + i] = run[i];
+  if (tid == 0) ch_last[c] = cur;
+  flush(cur);
+  if (tid == 0 && cnt_recs) atomicAdd((unsigned long long*)&ctl->rec_hist, cnt_recs);
+}
+
+// -------------------------------------------------------------- k_carry
+// Carry of each chunk's first segment from the earlier chunks: a segmented
+// scan over the chunks, one thread per digit (single CTA; 16 chunks in flight).
+static __global__ void __launch_bounds__(RADIX) k_carry(const uint32_t* __restrict__ ch_first, const uint32_t* __restrict__ ch_last,
+                                                 const uint32_t* __restrict__ ch_tot, uint32_t nch,
+                                                 uint32_t* __restrict__ carry_in) {
+  const int d = threadIdx.x;
+  uint32_t carry = 0, prev_last = NO_SEG;
+  constexpr int B = 16;
+  for (uint32_t c0 = 0; c0 < nch; c0 += B) {
+    uint32_t f[B], l[B], tt[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const uint32_t c = c0 + j;
+      f[j] = c < nch ? __ldg(ch_first + c) : NO_SEG;
+      l[j] = c < nch ? __ldg(ch_last + c) : NO_SEG;
+      tt[j] = c < nch ? __ldg(ch_tot + (size_t)c * RADIX + d) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const uint32_t c = c0 + j;
+      if (c >= nch || f[j] == NO_SEG) continue;
+      const uint32_t cin = (f[j] == prev_last) ? carry : 0u;
+      carry_in[(size_t)c * RADIX + d] = cin;
+      carry = (f[j] == l[j] ? cin : 0u) + tt[j];
+      prev_last = l[j];
+    }
+  }
+}
+
 // -------------------------------------------------------------- k_plan
 // Per Large segment: constant-digit skip / all-equal detection,
 // bin bases = exclusive prefix of the histogram.
@@ -254,11 +389,13 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __res
 // digit, obtain each digit's global offset by single-pass decoupled look-back
 // over the segment's tiles, and write every digit run with coalesced stores.
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
-template <int R, int K, int TB, int SB, int MINB>
+template <int R, int K, int TB, int SB, int MINB, bool PRE>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
-                                                       uint8_t* recs, uint8_t* tmp) {
+                                                       uint8_t* recs, uint8_t* tmp, const uint32_t* __restrict__ tile_pre,
+                                                       const uint32_t* __restrict__ ch_first,
+                                                       const uint32_t* __restrict__ carry_in, uint32_t hist_grid) {
   constexpr uint32_t T = (uint32_t)(TB / R);
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
@@ -313,6 +450,15 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     uint8_t* dst = buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
     if (sg.mode == MODE_SCATTER) {
       const uint32_t d = sg.depth;
+      uint32_t pre_excl = 0;
+      if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry), loaded early
+        if (tid < RADIX) {
+          const uint32_t per = (total + hist_grid - 1) / hist_grid;
+          const uint32_t ch = t / per;
+          pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) +
+                     (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
+        }
+      }
       uint32_t rk[I];
 #pragma unroll
       for (int i = 0; i < I; ++i) {
@@ -325,7 +471,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       unsigned long long* my = status + (size_t)t * RADIX + tid;
       if (tid < RADIX) {
         c = cnt[tid];
-        st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
+        if constexpr (!PRE) st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
       }
       if (tid == 0) take();  // next ticket, ready before the stage barrier
       const uint32_t ex = block_excl_scan256(c, ws);
@@ -344,7 +490,9 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       RS_PROF(3);
       if (tid < RADIX) {
         uint64_t excl = 0;
-        if (lt > 0) {
+        if constexpr (PRE) {
+          excl = pre_excl;
+        } else if (lt > 0) {
           // windowed decoupled look-back over this segment's earlier tiles
           uint32_t p = t - 1;
           for (;;) {

@@ -114,7 +114,8 @@ struct Sorter {
     set_attrs();
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
+      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
+      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
       attr = true;
     }
     Views v;
@@ -131,7 +132,25 @@ struct Sorter {
     const size_t tiles_max = v.tiles_max;
 
     int occ_s = 0, occ_h = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB>, SB, TB);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB, false>, SB, TB);
+    const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
+    const char* hg = getenv("RADSORT_HIST_CTAS_PER_SM");
+    const unsigned hist_grid = (unsigned)ctx->sms * (hg ? atoi(hg) : 4);  // chunks of the reduce-then-scan prefix
+    uint32_t* tile_pre = (uint32_t*)status;               // tiles x 256 u32 (status is tiles x 256 u64)
+    uint32_t* ch_first = (uint32_t*)ctx->mlo.p;
+    uint32_t* ch_last = (uint32_t*)ctx->mhi.p;
+    uint32_t* ch_tot = (uint32_t*)ctx->mlt.p;
+    uint32_t* carry_in = (uint32_t*)ctx->mle.p;
+    {
+      radsort_status rs2;
+      if ((rs2 = ensure(ctx->mlo, hist_grid * 4)) || (rs2 = ensure(ctx->mhi, hist_grid * 4)) ||
+          (rs2 = ensure(ctx->mlt, (size_t)hist_grid * RADIX * 4)) || (rs2 = ensure(ctx->mle, (size_t)hist_grid * RADIX * 4)))
+        return rs2;
+      ch_first = (uint32_t*)ctx->mlo.p;
+      ch_last = (uint32_t*)ctx->mhi.p;
+      ch_tot = (uint32_t*)ctx->mlt.p;
+      carry_in = (uint32_t*)ctx->mle.p;
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, TB>, HIST_B, 0);
     occ_s = std::max(occ_s, 1);
     occ_h = std::max(occ_h, 1);
@@ -164,7 +183,13 @@ struct Sorter {
         const size_t tiles_ub = std::min(tiles_max, (size_t)n / T + n_large + 1);
         const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
         tm.begin(RADSORT_K_HIST);
-        k_hist<R, K, TB><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
+        if (pre) {
+          k_hist_pre<R, K, TB><<<hist_grid, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp,
+                                                             tile_pre, ch_first, ch_last, ch_tot);
+          k_carry<<<1, RADIX, 0, st>>>(ch_first, ch_last, ch_tot, hist_grid, carry_in);
+        } else {
+          k_hist<R, K, TB><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
+        }
         tm.end();
         tm.begin(RADSORT_K_PLAN);
         k_plan<K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl);
@@ -175,8 +200,14 @@ struct Sorter {
         }
         const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
         tm.begin(RADSORT_K_SCATTER);
-        k_scatter<R, K, TB, SB, MINB><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status, ctx->epoch,
-                                                          ctl, recs, tmp);
+        if (pre)
+          k_scatter<R, K, TB, SB, MINB, true><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
+                                                                  ctx->epoch, ctl, recs, tmp, tile_pre, ch_first,
+                                                                  carry_in, hist_grid);
+        else
+          k_scatter<R, K, TB, SB, MINB, false><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
+                                                                   ctx->epoch, ctl, recs, tmp, nullptr, nullptr,
+                                                                   nullptr, 0);
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs, tmp);
@@ -291,8 +322,8 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   if (rs) return rs;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         MULTI_TB);
+    cudaFuncSetAttribute(k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, MULTI_TB);
     attr = true;
   }
   const Seg sg = {0u, n, (uint8_t)digit, SRC_REC, MODE_NONE, 0, 0};
@@ -308,11 +339,11 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
     ctx->epoch = 1;
   }
   int occ_s = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB>, MULTI_SB,
-                                                MULTI_TB);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false>,
+                                                MULTI_SB, MULTI_TB);
   const unsigned gs = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_s));
-  k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB><<<gs, MULTI_SB, MULTI_TB, st>>>(
-      v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp);
+  k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false><<<gs, MULTI_SB, MULTI_TB, st>>>(
+      v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, nullptr, nullptr, nullptr, 0);
   RS_CUDA(cudaGetLastError());
   RS_CUDA(cudaStreamSynchronize(st));
   workspace_release(ctx, st);
