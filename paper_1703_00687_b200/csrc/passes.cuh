@@ -664,7 +664,8 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
 // and queued for the next level.
 template <int R, int K, int IL>
 __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t stage_bytes,
-                                                      Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
+                                                      uint32_t sk_bytes, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs,
+                                                      uint8_t* tmp) {
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
   __shared__ uint32_t cnt[RADIX], start[RADIX], ws[8], big[RADIX];
@@ -673,6 +674,8 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
   constexpr int KW = K / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(stage + stage_bytes)[warp];
+  // compressed 32-bit sort keys for enumeration sort (0 bytes = disabled)
+  uint32_t* sk32 = reinterpret_cast<uint32_t*>(stage + stage_bytes + (LOCAL_B / 32) * sizeof(TailScratch<K>));
   uint32_t bi = blockIdx.x;
   if (bi >= nlist) return;
   Seg sg = list[bi];
@@ -698,7 +701,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
   prefetch_l2(bi + gridDim.x);
   if (tid < RADIX) cnt[tid] = 0;
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-  if (tid == 0) { nbig = 0; nsml = 0; }
+  if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
   unsigned long long done = 0;
 #ifdef RADSORT_PHASE_PROF
   unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = 0, tB = 0;
@@ -713,32 +716,60 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
     const uint32_t n = sg.len;
     uint8_t* out = recs + (size_t)sg.off * R;
     load(sg);
-    uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+    __syncthreads();  // counters / flags reset by the previous iteration are visible
+    // Optimistic digit: rank by the bin's next digit right away; only if that
+    // digit turns out constant over the bin (one sub-bin holds all n records)
+    // take the AND/OR of the keys and skip to the first non-constant digit
+    // (PAPER.md:38).  For uniform keys the reduction is never needed.
+    uint32_t d = sg.depth;
+    constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
+    uint32_t rk[IP];
+    auto rank_scan = [&](uint32_t dg) {
 #pragma unroll
-    for (int i = 0; i < IL; ++i) {
-      const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
-      if (idx < n) {
-        const Key<K> k = key_of<R, K>(r[i]);
-        na[0] |= ~k.w0; o[0] |= k.w0;
-        if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+      for (int i = 0; i < IP; ++i) rk[i] = 0;
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        if (idx < n) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), dg)], 1u) << (16 * (i & 1));
       }
-    }
-    __syncthreads();
+      __syncthreads();
+      const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
+      if (tid < RADIX && c > es_max<R>()) big[atomicAdd(&nbig, 1u)] = tid;  // sub-bins for phase B
+      if (tid < RADIX && c > 0 && c <= es_max<R>()) atomicAdd(&nsml, 1u);  // sub-bins for phase A
+      if (tid < RADIX && c == n) sh_d = 1u;                                  // digit constant over the bin
+      const uint32_t ex = block_excl_scan256(c, ws);
+      if (tid < RADIX) start[tid] = ex;
+    };
+    rank_scan(d);
+    if (sh_d) {  // rare: constant digit(s) -> AND/OR of the keys picks the next useful digit
+      uint64_t na[2] = {0, 0}, o[2] = {0, 0};
 #pragma unroll
-    for (int w = 0; w < KW; ++w) {
-      const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
-      const uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
-      const uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
-      const uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
-      if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
-    }
-    __syncthreads();
-    if (tid == 0) {
+      for (int i = 0; i < IL; ++i) {
+        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        if (idx < n) {
+          const Key<K> k = key_of<R, K>(r[i]);
+          na[0] |= ~k.w0; o[0] |= k.w0;
+          if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < KW; ++w) {
+        const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+        const uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+        const uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+        const uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+        if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
+      }
+      __syncthreads();
       uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
-      sh_d = first_nonconst_digit<K>(A, O, sg.depth);
+      d = first_nonconst_digit<K>(A, O, d);
+      __syncthreads();
+      if (tid < RADIX) cnt[tid] = 0;
+      if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
+      __syncthreads();
+      if (d < (uint32_t)K) rank_scan(d);
     }
     __syncthreads();
-    const uint32_t d = sh_d;
     RS_PROF(0);
     if (d >= (uint32_t)K) {  // all keys equal: final where it is (copied out of tmp)
       if (sg.src == SRC_TMP) {
@@ -749,22 +780,6 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
         }
       }
     } else {
-      constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
-      uint32_t rk[IP];
-#pragma unroll
-      for (int i = 0; i < IP; ++i) rk[i] = 0;
-#pragma unroll
-      for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
-        if (idx < n) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u) << (16 * (i & 1));
-      }
-      __syncthreads();
-      const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
-      if (tid < RADIX && c > es_max<R>()) big[atomicAdd(&nbig, 1u)] = tid;  // sub-bins for phase B
-      if (tid < RADIX && c > 0 && c <= es_max<R>()) atomicAdd(&nsml, 1u);  // sub-bins for phase A
-      const uint32_t ex = block_excl_scan256(c, ws);
-      if (tid < RADIX) start[tid] = ex;
-      __syncthreads();
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
@@ -780,7 +795,28 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       const uint32_t d1 = d + 1;
       RS_PROF(1);
       // phase A, record-parallel: singletons / exhausted digits copied, sub-bins
-      // of 2..ES_MAX records finished by enumeration sort
+      // of 2..ES_MAX records finished by enumeration sort.  When the bits left
+      // below the shared prefix fit in 24 bits (e.g. c2's last two digits), each
+      // record gets a 32-bit sort key (remaining key bits << 8 | slot in its
+      // sub-bin) and ES is one 32-bit compare per record pair.
+      const uint32_t rem_bits = 8u * ((uint32_t)K - d1);
+      // key = digit d (8 bits) | remaining key bits (16) | slot in sub-bin (8):
+      // ES then scans 16-byte-aligned windows and subtracts the records of the
+      // lower sub-bins that fall into the first window
+      const bool es32 = sk_bytes >= (n + 8u) * 4u && rem_bits <= 16u && nsml;
+      if (es32) {
+        for (uint32_t p = tid; p < ((n + 3u) & ~3u); p += LOCAL_B) {
+          uint32_t skv = 0xffffffffu;
+          if (p < n) {
+            const Key<K> kx = ld_key<R, K>(stage + (size_t)p * R);
+            const uint32_t v = digit_of(kx, d);
+            const uint32_t low = (uint32_t)kx.w0 & ((1u << rem_bits) - 1u);
+            skv = (v << 24) | (low << 8) | ((p - start[v]) & 255u);
+          }
+          sk32[p] = skv;
+        }
+        __syncthreads();
+      }
       for (uint32_t p = tid; p < (nsml || d1 >= (uint32_t)K ? n : 0u); p += LOCAL_B) {
         const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
         const Key<K> kx = key_of<R, K>(x);
@@ -789,7 +825,19 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
           st_rec<R>(out + (size_t)p * R, x);
         } else if (c <= es_max<R>()) {
           const uint32_t s0 = start[v];
-          st_rec<R>(out + (size_t)(s0 + es_rank<R, K>(stage + (size_t)s0 * R, c, p - s0, kx)) * R, x);
+          uint32_t rank;
+          if (es32) {
+            const uint32_t me = sk32[p];
+            const uint32_t a0 = s0 & ~3u, a1 = (s0 + c + 3u) & ~3u;
+            rank = a0 - s0;  // (mod 2^32) removes the lower sub-bins' records in the first window
+            for (uint32_t j = a0; j < a1; j += 4) {
+              const uint4 q = *reinterpret_cast<const uint4*>(sk32 + j);
+              rank += (uint32_t)(q.x < me) + (uint32_t)(q.y < me) + (uint32_t)(q.z < me) + (uint32_t)(q.w < me);
+            }
+          } else {
+            rank = es_rank<R, K>(stage + (size_t)s0 * R, c, p - s0, kx);
+          }
+          st_rec<R>(out + (size_t)(s0 + rank) * R, x);
         }
       }
       RS_PROF(2);
@@ -819,7 +867,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
     RS_PROF(4);
     if (tid < RADIX) cnt[tid] = 0;
     if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-    if (tid == 0) { nbig = 0; nsml = 0; }
+    if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
     if (nb >= nlist) break;
     bi = nb;
     sg = list[nb];

@@ -9,13 +9,15 @@ template <int R, int K>
 struct Sorter {
   static constexpr uint32_t C = local_capacity<R>();
   static constexpr int LOCAL_SCRATCH = (LOCAL_B / 32) * (int)sizeof(TailScratch<K>);
-  static constexpr int LOCAL_DYN_MAX = LOCAL_SMEM_BYTES + LOCAL_SCRATCH;
+  static constexpr int LOCAL_DYN_MAX = LOCAL_SMEM_BYTES + LOCAL_SCRATCH + 16384;
   static constexpr int CHILD_SCRATCH = (CHILD_B / 32) * (int)TINY_MAX * R;
 
   template <int IL>
   static void launch_local_t(uint32_t nloc, size_t stage_bytes, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                              uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
-    const size_t smem = stage_bytes + LOCAL_SCRATCH;
+    // 32-bit enumeration-sort keys for small bins (two CTAs per SM still fit)
+    const size_t sk_bytes = stage_bytes <= 65536 ? ((stage_bytes / R + 8) * 4 + 15) & ~(size_t)15 : 0;
+    const size_t smem = stage_bytes + LOCAL_SCRATCH + sk_bytes;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_local<R, K, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, LOCAL_DYN_MAX);
@@ -24,7 +26,8 @@ struct Sorter {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL>, LOCAL_B, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
-    k_local<R, K, IL><<<g, LOCAL_B, smem, st>>>(list, nloc, (uint32_t)stage_bytes, next, nxt, ctl, recs, tmp);
+    k_local<R, K, IL><<<g, LOCAL_B, smem, st>>>(list, nloc, (uint32_t)stage_bytes, (uint32_t)sk_bytes, next, nxt, ctl,
+                                                recs, tmp);
   }
 
   static void set_attrs() {
