@@ -662,8 +662,8 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
 // finished from smem by one warp: singletons / all-equal copied, <= TINY_MAX
 // sorted by warp_tail_sort (§3.3), larger ones written out
 // and queued for the next level.
-template <int R, int K, int IL>
-__global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t stage_bytes,
+template <int R, int K, int IL, int LB>
+__global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t stage_bytes,
                                                       uint32_t sk_bytes, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs,
                                                       uint8_t* tmp) {
   extern __shared__ uint4 smem_raw[];
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(stage + stage_bytes)[warp];
   // compressed 32-bit sort keys for enumeration sort (0 bytes = disabled)
-  uint32_t* sk32 = reinterpret_cast<uint32_t*>(stage + stage_bytes + (LOCAL_B / 32) * sizeof(TailScratch<K>));
+  uint32_t* sk32 = reinterpret_cast<uint32_t*>(stage + stage_bytes + (LB / 32) * sizeof(TailScratch<K>));
   uint32_t bi = blockIdx.x;
   if (bi >= nlist) return;
   Seg sg = list[bi];
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
     const uint8_t* src = buf_of(g.src, recs, tmp) + (size_t)g.off * R;
 #pragma unroll
     for (int i = 0; i < IL; ++i) {
-      const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+      const uint32_t idx = (uint32_t)(i * LB + tid);
       if (idx < g.len) r[i] = ldg_rec<R>(src + (size_t)idx * R);
     }
   };
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       for (int i = 0; i < IP; ++i) rk[i] = 0;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        const uint32_t idx = (uint32_t)(i * LB + tid);
         if (idx < n) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), dg)], 1u) << (16 * (i & 1));
       }
       __syncthreads();
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       uint64_t na[2] = {0, 0}, o[2] = {0, 0};
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        const uint32_t idx = (uint32_t)(i * LB + tid);
         if (idx < n) {
           const Key<K> k = key_of<R, K>(r[i]);
           na[0] |= ~k.w0; o[0] |= k.w0;
@@ -775,17 +775,28 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       if (sg.src == SRC_TMP) {
 #pragma unroll
         for (int i = 0; i < IL; ++i) {
-          const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+          const uint32_t idx = (uint32_t)(i * LB + tid);
           if (idx < n) st_rec<R>(out + (size_t)idx * R, r[i]);
         }
       }
     } else {
+      // ES keys for phase A are produced here too (slot in sub-bin = rank):
+      // digit (8) | key bits below the next digit (16) | slot (8)
+      const uint32_t rem_bits = 8u * ((uint32_t)K - d - 1u);
+      const bool es32 = sk_bytes >= (n + 8u) * 4u && rem_bits <= 16u;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LOCAL_B + tid);
+        const uint32_t idx = (uint32_t)(i * LB + tid);
         const uint32_t rki = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-        if (idx < n) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rki) * R, r[i]);
+        if (idx < n) {
+          const Key<K> kx = key_of<R, K>(r[i]);
+          const uint32_t v = digit_of(kx, d);
+          const uint32_t pos = start[v] + rki;
+          st_rec<R>(stage + (size_t)pos * R, r[i]);
+          if (es32) sk32[pos] = (v << 24) | (((uint32_t)kx.w0 & ((1u << rem_bits) - 1u)) << 8) | (rki & 255u);
+        }
       }
+      if (es32 && tid < 4) sk32[n + tid] = 0xffffffffu;  // window padding
       __syncthreads();
     }
     // the bin after next streams into L2 while this one is finished from smem
@@ -799,25 +810,11 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       // below the shared prefix fit in 24 bits (e.g. c2's last two digits), each
       // record gets a 32-bit sort key (remaining key bits << 8 | slot in its
       // sub-bin) and ES is one 32-bit compare per record pair.
-      const uint32_t rem_bits = 8u * ((uint32_t)K - d1);
-      // key = digit d (8 bits) | remaining key bits (16) | slot in sub-bin (8):
-      // ES then scans 16-byte-aligned windows and subtracts the records of the
-      // lower sub-bins that fall into the first window
-      const bool es32 = sk_bytes >= (n + 8u) * 4u && rem_bits <= 16u && nsml;
-      if (es32) {
-        for (uint32_t p = tid; p < ((n + 3u) & ~3u); p += LOCAL_B) {
-          uint32_t skv = 0xffffffffu;
-          if (p < n) {
-            const Key<K> kx = ld_key<R, K>(stage + (size_t)p * R);
-            const uint32_t v = digit_of(kx, d);
-            const uint32_t low = (uint32_t)kx.w0 & ((1u << rem_bits) - 1u);
-            skv = (v << 24) | (low << 8) | ((p - start[v]) & 255u);
-          }
-          sk32[p] = skv;
-        }
-        __syncthreads();
-      }
-      for (uint32_t p = tid; p < (nsml || d1 >= (uint32_t)K ? n : 0u); p += LOCAL_B) {
+      // ES keys (built while staging): one 32-bit compare per record pair, in
+      // 16-byte windows; the records of lower sub-bins in the first window are
+      // subtracted (their digit tag makes them compare below)
+      const bool es32 = sk_bytes >= (n + 8u) * 4u && 8u * ((uint32_t)K - d1) <= 16u;
+      for (uint32_t p = tid; p < (nsml || d1 >= (uint32_t)K ? n : 0u); p += LB) {
         const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
         const Key<K> kx = key_of<R, K>(x);
         const uint32_t v = digit_of(kx, d), c = cnt[v];
@@ -830,9 +827,14 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
             const uint32_t me = sk32[p];
             const uint32_t a0 = s0 & ~3u, a1 = (s0 + c + 3u) & ~3u;
             rank = a0 - s0;  // (mod 2^32) removes the lower sub-bins' records in the first window
-            for (uint32_t j = a0; j < a1; j += 4) {
-              const uint4 q = *reinterpret_cast<const uint4*>(sk32 + j);
-              rank += (uint32_t)(q.x < me) + (uint32_t)(q.y < me) + (uint32_t)(q.z < me) + (uint32_t)(q.w < me);
+            // c <= ES_MAX = 16 (24 for R = 32): at most 5 (7) windows, unrolled and predicated
+#pragma unroll
+            for (uint32_t w4 = 0; w4 < (es_max<R>() + 6u) / 4u; ++w4) {
+              const uint32_t j = a0 + 4u * w4;
+              if (j < a1) {
+                const uint4 q = *reinterpret_cast<const uint4*>(sk32 + j);
+                rank += (uint32_t)(q.x < me) + (uint32_t)(q.y < me) + (uint32_t)(q.z < me) + (uint32_t)(q.w < me);
+              }
             }
           } else {
             rank = es_rank<R, K>(stage + (size_t)s0 * R, c, p - s0, kx);
@@ -844,7 +846,7 @@ __global__ void __launch_bounds__(LOCAL_B, (IL * R <= 128) ? 2 : 1) k_local(cons
       // phase B, one warp per larger sub-bin
       if (d1 < (uint32_t)K) {
         const uint32_t nb_ = nbig;
-        for (uint32_t q = warp; q < nb_; q += LOCAL_B / 32) {
+        for (uint32_t q = warp; q < nb_; q += LB / 32) {
           const uint32_t v = big[q];
           const uint32_t len = cnt[v];
           const uint32_t o0 = start[v];

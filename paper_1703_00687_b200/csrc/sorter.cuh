@@ -12,22 +12,22 @@ struct Sorter {
   static constexpr int LOCAL_DYN_MAX = LOCAL_SMEM_BYTES + LOCAL_SCRATCH + 16384;
   static constexpr int CHILD_SCRATCH = (CHILD_B / 32) * (int)TINY_MAX * R;
 
-  template <int IL>
+  template <int IL, int LB>
   static void launch_local_t(uint32_t nloc, size_t stage_bytes, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                              uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
     // 32-bit enumeration-sort keys for small bins (two CTAs per SM still fit)
     const size_t sk_bytes = stage_bytes <= 65536 ? ((stage_bytes / R + 8) * 4 + 15) & ~(size_t)15 : 0;
-    const size_t smem = stage_bytes + LOCAL_SCRATCH + sk_bytes;
+    const size_t smem = stage_bytes + (LB / 32) * sizeof(TailScratch<K>) + sk_bytes;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_local<R, K, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, LOCAL_DYN_MAX);
+      cudaFuncSetAttribute(k_local<R, K, IL, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, LOCAL_DYN_MAX);
       attr = true;
     }
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL>, LOCAL_B, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
-    k_local<R, K, IL><<<g, LOCAL_B, smem, st>>>(list, nloc, (uint32_t)stage_bytes, (uint32_t)sk_bytes, next, nxt, ctl,
-                                                recs, tmp);
+    k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, (uint32_t)stage_bytes, (uint32_t)sk_bytes, next, nxt, ctl,
+                                               recs, tmp);
   }
 
   static void set_attrs() {
@@ -40,9 +40,9 @@ struct Sorter {
   // Local bins of up to `maxlen` records: IL = records per thread.
   static void launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                            uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
-    const uint32_t il = (maxlen + LOCAL_B - 1) / LOCAL_B;
     const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
-#define RS_LOCAL(IL) launch_local_t<IL>(nloc, stage_bytes, list, next, nxt, ctl, recs, tmp, st, sms)
+    const uint32_t il = (maxlen + LOCAL_B - 1) / LOCAL_B;
+#define RS_LOCAL(IL) launch_local_t<IL, LOCAL_B>(nloc, stage_bytes, list, next, nxt, ctl, recs, tmp, st, sms)
     if (il <= 1) RS_LOCAL(1);
     else if (il <= 2) RS_LOCAL(2);
     else if (il <= 4) RS_LOCAL(4);
