@@ -101,12 +101,13 @@ struct Sorter {
   static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
                             radsort_stats& stats) {
     const char* e = getenv("RADSORT_SCATTER_CFG");
-    const int cfg = e ? atoi(e) : 0;
+    const int cfg = e ? atoi(e) : 1;
     switch (cfg) {
-      case 1: return run_cfg<32768, 256, 4>(ctx, recs, tmp, n, st, stats);
+      case 0: return run_cfg<65536, 512, 2>(ctx, recs, tmp, n, st, stats);
       case 2: return run_cfg<32768, 512, 2>(ctx, recs, tmp, n, st, stats);
       case 3: return run_cfg<16384, 256, 4>(ctx, recs, tmp, n, st, stats);
-      default: return run_cfg<65536, 512, 2>(ctx, recs, tmp, n, st, stats);
+      case 4: return run_cfg<49152, 384, 3>(ctx, recs, tmp, n, st, stats);
+      default: return run_cfg<32768, 256, 4>(ctx, recs, tmp, n, st, stats);  // measured best
     }
   }
 

@@ -25,7 +25,7 @@ def C_of(R):
 
 
 def T_of(R):
-    return 65536 // R
+    return 32768 // R  # default scatter tile (RADSORT_SCATTER_CFG=1)
 
 
 def run_gpu_sort(a: np.ndarray, K: int, guard=True):
@@ -73,8 +73,20 @@ def test_small_sizes(R, K, n):
 @pytest.mark.parametrize("R,K", LAYOUTS)
 def test_capacity_and_tile_boundaries(R, K):
     C, T = C_of(R), T_of(R)
-    for n in (C - 1, C, C + 1, T - 1, T + 1, 3 * T + 17):
+    for n in (C - 1, C, C + 1, T - 1, T + 1, 3 * T + 17, 2 * 65536 // R + 5):
         check(dg.generate(n, R, K, "uniform", seed=n), K)
+
+
+@pytest.mark.parametrize("cfg", ["0", "2", "3", "4"])
+def test_other_tile_configs(cfg, monkeypatch):
+    # every scatter/histogram tile configuration and the look-back variant stay exact
+    monkeypatch.setenv("RADSORT_SCATTER_CFG", cfg)
+    for R, K in ((8, 8), (16, 8), (32, 16)):
+        check(dg.generate(400_003, R, K, "uniform", seed=11), K)
+        check(dg.generate(200_001, R, K, "few", payload="index" if R > K else "random", seed=12), K)
+    monkeypatch.setenv("RADSORT_LOOKBACK", "1")
+    for R, K in ((8, 8), (16, 8), (32, 16)):
+        check(dg.generate(400_003, R, K, "zipf", seed=13), K)
 
 
 @pytest.mark.parametrize("R,K", LAYOUTS)
