@@ -254,14 +254,32 @@ def run_radsort(args):
     passes_bytes = sum(kern_bytes.values()) / args.steps  # algorithmic bytes per step (read + write)
     eff_gbs = passes_bytes * world / (total_ms / args.steps / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
-    sc_ms = kern_ms.get("scatter", 0.0)
-    sc_bytes = kern_bytes.get("scatter", 0)
-    achieved = sc_bytes / (sc_ms / 1e3) / 1e9 if sc_ms > 0 else None
-    traffic = None
+    # roofline of the dominant HBM-bound kernel (largest time per step), with
+    # the traffic ncu measured for it (profiles/traffic_<config>.json, bytes per launch)
+    traffic_map = {}
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("scatter_bytes_per_launch")
+            traffic_map = json.load(f)
+    names = {"scatter": "k_scatter (radix pass: rank, smem staging, coalesced scatter)",
+             "local": "k_local (CTA-local smem sort of bins <= C records)",
+             "hist": "k_hist_pre (digit histogram + per-tile prefix, read only)"}
+    launches_per_step = {k: v for k, v in rs.last_stats()["kernel_launches"].items()}
+    roof_all = {}
+    for k in ("scatter", "local", "hist"):
+        ms = kern_ms.get(k, 0.0)
+        b = kern_bytes.get(k, 0)
+        if ms <= 0 or b <= 0:
+            continue
+        ach = b / (ms / 1e3) / 1e9
+        nl = max(1, launches_per_step.get(k, 1))
+        tr = traffic_map.get(k)
+        roof_all[k] = {"bound": "hbm", "kernel": names[k], "achieved": round(ach, 1), "peak": peak,
+                       "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
+                       "traffic": tr, "bytes_per_launch": b / args.steps / nl, "launches_per_step": nl,
+                       "ms_per_step": round(ms / args.steps, 4)}
+    dom = max(roof_all, key=lambda k: roof_all[k]["ms_per_step"]) if roof_all else None
+    roofline = dict(roof_all[dom]) if dom else None
 
     # end to end through the public C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -296,11 +314,8 @@ def run_radsort(args):
                        "l2": "inputs larger than the 126 MB L2; input restored from a pristine copy between steps"},
             "effective_hbm_gbs": round(eff_gbs, 1),
             "hbm_frac_of_8tbs": round(eff_gbs / 8000.0, 4),
-            "roofline": {"bound": "hbm", "kernel": "k_scatter (look-back radix pass)",
-                         "achieved": round(achieved, 1) if achieved else None, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
-                         "bytes_per_step": sc_bytes / args.steps, "ms_per_step": sc_ms / args.steps},
+            "roofline": roofline,
+            "roofline_by_kernel": roof_all,
             "kernel_ms_per_step": {k: round(v / args.steps, 4) for k, v in kern_ms.items()},
             "kernel_bytes_per_step": {k: v // args.steps for k, v in kern_bytes.items()},
             "passes": {"levels": stats["levels"], "scatter_passes": stats["scatter_passes"],

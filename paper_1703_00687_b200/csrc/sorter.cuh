@@ -217,7 +217,7 @@ struct Sorter {
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs, tmp);
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
-        stats.kernel_launches[RADSORT_K_HIST]++;
+        stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry
         stats.kernel_launches[RADSORT_K_SCATTER]++;
         stats.kernel_launches[RADSORT_K_CHILDREN]++;
         stats.scatter_passes++;
