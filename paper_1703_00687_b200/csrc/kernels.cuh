@@ -430,13 +430,14 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
     if (i < n) {
       const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
       uint32_t fin = slot;
-      if (c == 2) {  // the common collision: one comparison with the partner
-        const uint32_t other = 2 * s0 + 1 - slot;
-        const Key<K> kq = ws.key[other];
-        fin = s0 + ((uint32_t)key_lt(kq, k[e]) | ((uint32_t)(other < slot) & (uint32_t)key_eq(kq, k[e])));
-      } else if (c > 2) {
+      if (c > 1) {  // ES among the sub-bin's c records (pairs / triples: predicated, no divergent loop)
         uint32_t r = 0;
-        for (uint32_t q = s0; q < s0 + c; ++q) {
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          const Key<K> kq = ws.key[min(s0 + q, (uint32_t)TINY_MAX - 1u)];
+          r += (uint32_t)(q < c) & ((uint32_t)key_lt(kq, k[e]) | ((uint32_t)(s0 + q < slot) & (uint32_t)key_eq(kq, k[e])));
+        }
+        for (uint32_t q = s0 + 4; q < s0 + c; ++q) {
           const Key<K> kq = ws.key[q];
           r += (uint32_t)key_lt(kq, k[e]) | ((uint32_t)(q < slot) & (uint32_t)key_eq(kq, k[e]));
         }
