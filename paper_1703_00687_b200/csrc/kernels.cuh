@@ -420,17 +420,34 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
       const uint32_t w = ws.cnt[digit_of(k[e], depth)];
       const uint32_t slot = (w >> 16) + pr[e];
       ws.key[slot] = k[e];
-      pr[e] = slot | ((w >> 16) << 8) | ((w & 0xffffu) << 16);  // slot | start << 8 | count << 16
+      pr[e] = slot | ((w >> 16) << 8) | ((w & 0xffu) << 16);  // slot | start << 8 | count << 16
     }
   }
   __syncwarp();
+  // sub-bins whose records all carry the same key need no ordering (PAPER.md:38
+  // "bins with all keys equal"): flag (bit 15 of the packed counter) the ones
+  // holding a key different from their first record's
+  bool big = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) big |= ((uint32_t)(e * 32 + lane) < n) && (pr[e] >> 16) > 4u;
+  const bool checked = __any_sync(0xffffffffu, big);
+  if (checked) {  // only sub-bins of > 4 records are worth the check
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = (uint32_t)(e * 32 + lane);
+      if (i < n && (pr[e] >> 16) > 1u && !key_eq(ws.key[(pr[e] >> 8) & 0xffu], k[e]))
+        atomicOr(&ws.cnt[digit_of(k[e], depth)], 0x8000u);
+    }
+    __syncwarp();
+  }
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const uint32_t i = (uint32_t)(e * 32 + lane);
     if (i < n) {
       const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
       uint32_t fin = slot;
-      if (c > 1) {  // ES among the sub-bin's c records (pairs / triples: predicated, no divergent loop)
+      const bool mixed = !checked || (ws.cnt[digit_of(k[e], depth)] & 0x8000u) != 0u;
+      if (c > 1 && mixed) {  // ES among the sub-bin's c records (pairs / triples: predicated, no divergent loop)
         uint32_t r = 0;
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
