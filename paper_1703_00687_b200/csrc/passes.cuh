@@ -709,13 +709,17 @@ __global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_lo
 #else
 #define RS_PROF(i) do { } while (0)
 #endif
+  // big bins (one CTA per SM) load the next bin while finishing the current one;
+  // small bins rely on the second resident CTA instead (fewer live registers)
+  constexpr bool PIPE = IL * R >= 256;
+  if (PIPE) load(sg);
   for (;;) {
 #ifdef RADSORT_PHASE_PROF
     if (tid == 0) { tA = clock64(); pf[7]++; }
 #endif
     const uint32_t n = sg.len;
     uint8_t* out = recs + (size_t)sg.off * R;
-    load(sg);
+    if (!PIPE) load(sg);
     __syncthreads();  // counters / flags reset by the previous iteration are visible
     // Optimistic digit: rank by the bin's next digit right away; only if that
     // digit turns out constant over the bin (one sub-bin holds all n records)
@@ -802,6 +806,13 @@ __global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_lo
     // the bin after next streams into L2 while this one is finished from smem
     const uint32_t nb = bi + gridDim.x;
     prefetch_l2(nb + gridDim.x);
+    // registers are free once the bin is staged: start loading the next bin now
+    // so its latency overlaps this bin's finishing phases
+    Seg nsg = sg;
+    if (nb < nlist) {
+      nsg = list[nb];
+      if (PIPE) load(nsg);
+    }
     if (d < (uint32_t)K) {
       const uint32_t d1 = d + 1;
       RS_PROF(1);
@@ -872,7 +883,7 @@ __global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_lo
     if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
     if (nb >= nlist) break;
     bi = nb;
-    sg = list[nb];
+    sg = nsg;
   }
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
 #ifdef RADSORT_PHASE_PROF
