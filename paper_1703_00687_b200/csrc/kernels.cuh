@@ -17,7 +17,6 @@ namespace radsort {
 constexpr int RADIX = 256;
 constexpr uint32_t TINY_MAX = 128;     // warp tiny sorter ceiling ("up to about a hundred")
 constexpr int HIST_B = 256;            // threads per histogram CTA
-constexpr int LOCAL_B = 512;           // threads per CTA-local sorter
 constexpr int CHILD_B = 256;           // threads per children CTA
 constexpr int LOCAL_SMEM_BYTES = 131072;  // CTA-local sorter capacity in bytes
 

@@ -655,30 +655,135 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
 // -------------------------------------------------------------- k_local
 // CTA-local sort of bins of <= C records (the GPU analog of PAPER.md:134
 // §3.2 "the bin is small enough to fit in a half of L2 ... simple counting
-// and scatter").  Persistent CTAs walk the Local list; for each bin: records
-// in registers -> block AND/OR picks the first non-constant digit (constant
-// digits skipped) -> counting scatter into shared memory -> the
-// bin after next is prefetched into L2 by a TMA bulk prefetch -> every sub-bin is
-// finished from smem by one warp: singletons / all-equal copied, <= TINY_MAX
-// sorted by warp_tail_sort (§3.3), larger ones written out
-// and queued for the next level.
-template <int R, int K, int IL, int LB>
-__global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t stage_bytes,
-                                                      uint32_t sk_bytes, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs,
-                                                      uint8_t* tmp) {
-  extern __shared__ uint4 smem_raw[];
-  uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
-  __shared__ uint32_t cnt[RADIX], start[RADIX], ws[8], big[RADIX];
-  __shared__ unsigned long long sna[2], so[2];
-  __shared__ uint32_t sh_d, nbig, nsml;
-  constexpr int KW = K / 8;
+// and scatter", and of PAPER.md:181-183 §3.3 for what is left inside it).
+//
+// Per bin, with the bin's records in registers:
+//  1. counting pass on a composite digit of W bits -- digit d followed by the
+//     leading W-8 bits of digit d+1 (W = log2(bin)+1, 10..16; DESIGN.md §4:
+//     one smem counting pass that does the work of up to two MSD levels) --
+//     u16 counters, two per word, ranks from smem atomics;
+//  2. exclusive scan of the counters (warp-cooperative, 16-byte accesses);
+//     a bucket holding the whole bin means constant leading digits: the AND/OR
+//     of the keys picks the first non-constant digit and the pass
+//     is redone there, or the bin is final when all keys are equal;
+//  3. every record is stored to smem at its bucket position, and the next
+//     bin's loads are issued right away (registers are free again);
+//  4. write-out, one coalesced pass over the staged bin: a record alone in its
+//     bucket is final; the records of a bucket of 2..ES_MAX get their place by
+//     enumeration sort on the full key among that bucket only (PAPER.md:102-104
+//     ES; ties by staged position); a larger bucket holding a single key is
+//     final as staged ("bins with all keys equal");
+//  5. larger buckets holding several keys (only duplicated or skewed keys
+//     produce them): <= TINY_MAX records by the warp tail sorter, larger ones
+//     are written out and queued as Local bins of the next level.
+// Writes stay coalesced: a warp writes 32 consecutive staged records, each
+// to a place inside its own (small) bucket.
+constexpr uint32_t LOCAL_WMIN = 10;  // narrowest composite digit: 2^(W-1) >= 512 counter words
+
+// Bucket of a key at depth d (< K): the top W bits of the key bits below its
+// d leading digits (zero bits past the end of the key).
+__device__ __forceinline__ uint32_t bucket_of(const Key<8>& k, uint32_t d, uint32_t W) {
+  return (uint32_t)((k.w0 << (8u * d)) >> (64u - W));
+}
+__device__ __forceinline__ uint32_t bucket_of(const Key<16>& k, uint32_t d, uint32_t W) {
+  const uint32_t s = 8u * d;
+  uint64_t x;
+  if (s == 0) x = k.w1;
+  else if (s < 64) x = (k.w1 << s) | (k.w0 >> (64u - s));
+  else x = k.w0 << (s - 64u);
+  return (uint32_t)(x >> (64u - W));
+}
+
+__host__ __device__ __forceinline__ uint32_t local_width(uint32_t n, uint32_t wmax) {
+  uint32_t w = 1;
+  while ((1u << w) < n) ++w;  // ceil(log2 n)
+  w += 1;
+  return w < LOCAL_WMIN ? LOCAL_WMIN : (w > wmax ? wmax : w);
+}
+
+// In-place exclusive scan of the 2^W u16 bucket counters (two per word): one
+// contiguous chunk per warp, 16-byte accesses.  Buckets with more than `es`
+// records are appended to `big` as {bucket, start | count << 16}; *s_const is
+// set when a bucket holds all n records.  Contains one block barrier; the
+// caller synchronises after it.
+template <int LB>
+__device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t n, uint32_t es, uint2* big,
+                                           uint32_t* s_nbig, uint32_t* s_const, uint32_t* wsum) {
+  constexpr int NW = LB / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(stage + stage_bytes)[warp];
-  // compressed 32-bit sort keys for enumeration sort (0 bytes = disabled)
-  uint32_t* sk32 = reinterpret_cast<uint32_t*>(stage + stage_bytes + (LB / 32) * sizeof(TailScratch<K>));
+  const uint32_t pw = (1u << (W - 1)) / NW;  // words per warp, a multiple of 4
+  const uint32_t n4 = pw / 4;
+  uint4* c4 = reinterpret_cast<uint4*>(cnt + (size_t)warp * pw);
+  uint32_t tot = 0;
+  for (uint32_t j = lane; j < n4; j += 32) {
+    const uint4 v = c4[j];
+    tot += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) + (v.z & 0xffffu) + (v.z >> 16) +
+           (v.w & 0xffffu) + (v.w >> 16);
+  }
+  tot = __reduce_add_sync(0xffffffffu, tot);
+  if (lane == 0) wsum[warp] = tot;
+  __syncthreads();
+  uint32_t carry = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) carry += (w < warp) ? wsum[w] : 0u;
+  for (uint32_t j0 = 0; j0 < n4; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    const uint4 v = j < n4 ? c4[j] : make_uint4(0, 0, 0, 0);
+    const uint32_t c[8] = {v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16,
+                           v.z & 0xffffu, v.z >> 16, v.w & 0xffffu, v.w >> 16};
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += c[k];
+    uint32_t inc = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    uint32_t s = carry + inc - t;
+    uint32_t st[8];
+    bool any_big = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      st[k] = s;
+      s += c[k];
+      any_big |= c[k] > es;
+    }
+    if (any_big) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (c[k] > es) {
+          if (c[k] == n) *s_const = 1u;
+          const uint32_t b = 2u * (warp * pw + 4u * j) + (uint32_t)k;
+          big[atomicAdd(s_nbig, 1u)] = make_uint2(b, st[k] | (c[k] << 16));
+        }
+      }
+    }
+    if (j < n4) c4[j] = make_uint4(st[0] | (st[1] << 16), st[2] | (st[3] << 16), st[4] | (st[5] << 16), st[6] | (st[7] << 16));
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
+template <int R, int K, int IL, int LB>
+__global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
+    k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes, uint32_t cnt_bytes,
+            Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
+  extern __shared__ uint4 smem_raw[];
+  constexpr int KW = K / 8;
+  constexpr uint32_t ES = es_max<R>();
+  uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + stage_bytes);              // 2^W u16 counters
+  uint2* big = reinterpret_cast<uint2*>(stage + stage_bytes + cnt_bytes);        // buckets of > ES records
+  __shared__ uint32_t wsum[LB / 32], s_nbig, s_const;
+  __shared__ unsigned long long sna[2], so[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(cnt)[warp];  // aliases cnt in phase 5 only
   uint32_t bi = blockIdx.x;
   if (bi >= nlist) return;
-  Seg sg = list[bi];
+  auto zero_cnt = [&](uint32_t bytes) {
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (uint32_t i = tid; i < bytes / 16u; i += LB) c4[i] = make_uint4(0, 0, 0, 0);
+  };
   Rec<R> r[IL];
   auto load = [&](const Seg& g) {
     const uint8_t* src = buf_of(g.src, recs, tmp) + (size_t)g.off * R;
@@ -698,54 +803,40 @@ __global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_lo
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s1), "r"((uint32_t)(e1 - s1)) : "memory");
     }
   };
+  Seg sg = list[bi];
+  load(sg);
   prefetch_l2(bi + gridDim.x);
-  if (tid < RADIX) cnt[tid] = 0;
+  zero_cnt(cnt_bytes);
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-  if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
+  if (tid == 0) { s_nbig = 0; s_const = 0; }
   unsigned long long done = 0;
-#ifdef RADSORT_PHASE_PROF
-  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = 0, tB = 0;
-#define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
-#else
-#define RS_PROF(i) do { } while (0)
-#endif
-  // big bins (one CTA per SM) load the next bin while finishing the current one;
-  // small bins rely on the second resident CTA instead (fewer live registers)
-  constexpr bool PIPE = IL * R >= 256;
-  if (PIPE) load(sg);
+  constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
   for (;;) {
-#ifdef RADSORT_PHASE_PROF
-    if (tid == 0) { tA = clock64(); pf[7]++; }
-#endif
     const uint32_t n = sg.len;
     uint8_t* out = recs + (size_t)sg.off * R;
-    if (!PIPE) load(sg);
-    __syncthreads();  // counters / flags reset by the previous iteration are visible
-    // Optimistic digit: rank by the bin's next digit right away; only if that
-    // digit turns out constant over the bin (one sub-bin holds all n records)
-    // take the AND/OR of the keys and skip to the first non-constant digit
-    // (PAPER.md:38).  For uniform keys the reduction is never needed.
     uint32_t d = sg.depth;
-    constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
+    uint32_t W = local_width(n, wmax);
     uint32_t rk[IP];
-    auto rank_scan = [&](uint32_t dg) {
+    bool all_equal = false;
+    __syncthreads();  // counters zero, flags reset
+    for (;;) {  // one round unless the composite digit is constant over the bin
 #pragma unroll
       for (int i = 0; i < IP; ++i) rk[i] = 0;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         const uint32_t idx = (uint32_t)(i * LB + tid);
-        if (idx < n) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), dg)], 1u) << (16 * (i & 1));
+        if (idx < n) {
+          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t sh = 16u * (b & 1u);
+          const uint32_t old = atomicAdd(&cnt[b >> 1], 1u << sh);
+          rk[i >> 1] |= ((old >> sh) & 0xffffu) << (16 * (i & 1));
+        }
       }
       __syncthreads();
-      const uint32_t c = tid < RADIX ? cnt[tid] : 0u;
-      if (tid < RADIX && c > es_max<R>()) big[atomicAdd(&nbig, 1u)] = tid;  // sub-bins for phase B
-      if (tid < RADIX && c > 0 && c <= es_max<R>()) atomicAdd(&nsml, 1u);  // sub-bins for phase A
-      if (tid < RADIX && c == n) sh_d = 1u;                                  // digit constant over the bin
-      const uint32_t ex = block_excl_scan256(c, ws);
-      if (tid < RADIX) start[tid] = ex;
-    };
-    rank_scan(d);
-    if (sh_d) {  // rare: constant digit(s) -> AND/OR of the keys picks the next useful digit
+      local_scan<LB>(cnt, W, n, ES, big, &s_nbig, &s_const, wsum);
+      __syncthreads();
+      if (!s_const) break;
+      // every record in one bucket: skip the constant digits
       uint64_t na[2] = {0, 0}, o[2] = {0, 0};
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
@@ -766,16 +857,16 @@ __global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_lo
       }
       __syncthreads();
       uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
-      d = first_nonconst_digit<K>(A, O, d);
+      const uint32_t d2 = first_nonconst_digit<K>(A, O, d);
       __syncthreads();
-      if (tid < RADIX) cnt[tid] = 0;
-      if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
+      zero_cnt(2u << W);
+      if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+      if (tid == 0) { s_nbig = 0; s_const = 0; }
       __syncthreads();
-      if (d < (uint32_t)K) rank_scan(d);
+      if (d2 >= (uint32_t)K) { all_equal = true; break; }
+      d = d2;
     }
-    __syncthreads();
-    RS_PROF(0);
-    if (d >= (uint32_t)K) {  // all keys equal: final where it is (copied out of tmp)
+    if (all_equal) {  // final where it is (copied out of tmp)
       if (sg.src == SRC_TMP) {
 #pragma unroll
         for (int i = 0; i < IL; ++i) {
@@ -784,116 +875,100 @@ __global__ void __launch_bounds__(LB, (LB <= 512 && IL * R <= 128) ? 2 : 1) k_lo
         }
       }
     } else {
-      // ES keys for phase A are produced here too (slot in sub-bin = rank):
-      // digit (8) | key bits below the next digit (16) | slot (8)
-      const uint32_t rem_bits = 8u * ((uint32_t)K - d - 1u);
-      const bool es32 = sk_bytes >= (n + 8u) * 4u && rem_bits <= 16u;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         const uint32_t idx = (uint32_t)(i * LB + tid);
-        const uint32_t rki = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
         if (idx < n) {
-          const Key<K> kx = key_of<R, K>(r[i]);
-          const uint32_t v = digit_of(kx, d);
-          const uint32_t pos = start[v] + rki;
-          st_rec<R>(stage + (size_t)pos * R, r[i]);
-          if (es32) sk32[pos] = (v << 24) | (((uint32_t)kx.w0 & ((1u << rem_bits) - 1u)) << 8) | (rki & 255u);
+          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t s = (cnt[b >> 1] >> (16u * (b & 1u))) & 0x7fffu;
+          st_rec<R>(stage + (size_t)(s + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)) * R, r[i]);
         }
       }
-      if (es32 && tid < 4) sk32[n + tid] = 0xffffffffu;  // window padding
-      __syncthreads();
     }
-    // the bin after next streams into L2 while this one is finished from smem
+    // registers are free: the next bin's loads overlap this bin's write-out;
+    // the bin after next streams into L2
     const uint32_t nb = bi + gridDim.x;
-    prefetch_l2(nb + gridDim.x);
-    // registers are free once the bin is staged: start loading the next bin now
-    // so its latency overlaps this bin's finishing phases
     Seg nsg = sg;
     if (nb < nlist) {
       nsg = list[nb];
-      if (PIPE) load(nsg);
+      load(nsg);
     }
-    if (d < (uint32_t)K) {
-      const uint32_t d1 = d + 1;
-      RS_PROF(1);
-      // phase A, record-parallel: singletons / exhausted digits copied, sub-bins
-      // of 2..ES_MAX records finished by enumeration sort.  When the bits left
-      // below the shared prefix fit in 24 bits (e.g. c2's last two digits), each
-      // record gets a 32-bit sort key (remaining key bits << 8 | slot in its
-      // sub-bin) and ES is one 32-bit compare per record pair.
-      // ES keys (built while staging): one 32-bit compare per record pair, in
-      // 16-byte windows; the records of lower sub-bins in the first window are
-      // subtracted (their digit tag makes them compare below)
-      const bool es32 = sk_bytes >= (n + 8u) * 4u && 8u * ((uint32_t)K - d1) <= 16u;
-      for (uint32_t p = tid; p < (nsml || d1 >= (uint32_t)K ? n : 0u); p += LB) {
-        const Rec<R> x = ld_rec<R>(stage + (size_t)p * R);
-        const Key<K> kx = key_of<R, K>(x);
-        const uint32_t v = digit_of(kx, d), c = cnt[v];
-        if (c == 1 || d1 >= (uint32_t)K) {
-          st_rec<R>(out + (size_t)p * R, x);
-        } else if (c <= es_max<R>()) {
-          const uint32_t s0 = start[v];
-          uint32_t rank;
-          if (es32) {
-            const uint32_t me = sk32[p];
-            const uint32_t a0 = s0 & ~3u, a1 = (s0 + c + 3u) & ~3u;
-            rank = a0 - s0;  // (mod 2^32) removes the lower sub-bins' records in the first window
-            // c <= ES_MAX = 16 (24 for R = 32): at most 5 (7) windows, unrolled and predicated
-#pragma unroll
-            for (uint32_t w4 = 0; w4 < (es_max<R>() + 6u) / 4u; ++w4) {
-              const uint32_t j = a0 + 4u * w4;
-              if (j < a1) {
-                const uint4 q = *reinterpret_cast<const uint4*>(sk32 + j);
-                rank += (uint32_t)(q.x < me) + (uint32_t)(q.y < me) + (uint32_t)(q.z < me) + (uint32_t)(q.w < me);
-              }
-            }
-          } else {
-            rank = es_rank<R, K>(stage + (size_t)s0 * R, c, p - s0, kx);
-          }
-          st_rec<R>(out + (size_t)(s0 + rank) * R, x);
+    prefetch_l2(nb + gridDim.x);
+    bool tail = false;
+    if (!all_equal) {
+      const uint32_t nbk = 1u << W;
+      const int rem = 8 * ((int)K - (int)d) - (int)W;  // key bits below the composite digit
+      auto start_of = [&](uint32_t b) { return (cnt[b >> 1] >> (16u * (b & 1u))) & 0xffffu; };
+      const uint32_t nbig = s_nbig;
+      __syncthreads();
+      if (nbig && rem > 0) {  // flag the big buckets that hold more than one key
+        for (uint32_t q = tid; q < n; q += LB) {
+          const Key<K> kx = ld_key<R, K>(stage + (size_t)q * R);
+          const uint32_t b = bucket_of(kx, d, W);
+          const uint32_t s0 = start_of(b) & 0x7fffu, s1 = b + 1 < nbk ? start_of(b + 1) & 0x7fffu : n;
+          if (s1 - s0 > ES && !key_eq(ld_key<R, K>(stage + (size_t)s0 * R), kx))
+            atomicOr(&cnt[b >> 1], 0x8000u << (16u * (b & 1u)));
         }
+        __syncthreads();
       }
-      RS_PROF(2);
-      // phase B, one warp per larger sub-bin
-      if (d1 < (uint32_t)K) {
-        const uint32_t nb_ = nbig;
-        for (uint32_t q = warp; q < nb_; q += LB / 32) {
-          const uint32_t v = big[q];
-          const uint32_t len = cnt[v];
-          const uint32_t o0 = start[v];
-          if (len <= TINY_MAX) {
-            warp_tail_sort<R, K>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, d1, lane, tsc);
+      for (uint32_t q = tid; q < n; q += LB) {
+        const Rec<R> x = ld_rec<R>(stage + (size_t)q * R);
+        uint32_t dest = q;
+        if (rem > 0) {
+          const Key<K> kx = key_of<R, K>(x);
+          const uint32_t b = bucket_of(kx, d, W);
+          const uint32_t w0 = start_of(b);
+          const uint32_t s0 = w0 & 0x7fffu, s1 = b + 1 < nbk ? start_of(b + 1) & 0x7fffu : n;
+          const uint32_t c = s1 - s0;
+          if (c > ES) {
+            if (w0 & 0x8000u) continue;  // several keys: phase 5
+          } else if (c > 1) {            // enumeration sort inside the bucket
+            uint32_t rank = 0;
+            for (uint32_t j = s0; j < s1; ++j) {
+              const Key<K> kj = ld_key<R, K>(stage + (size_t)j * R);
+              rank += (uint32_t)key_lt(kj, kx) | ((uint32_t)(j < q) & (uint32_t)key_eq(kj, kx));
+            }
+            dest = s0 + rank;
+          }
+        }
+        st_rec<R>(out + (size_t)dest * R, x);
+      }
+      if (nbig && rem > 0) {
+        __syncthreads();  // counters no longer read: mark mixed big buckets, then reuse cnt as tail scratch
+        for (uint32_t e = tid; e < nbig; e += LB) {
+          const uint32_t b = big[e].x;
+          if (start_of(b) & 0x8000u) big[e].x = b | 0x80000000u;
+        }
+        __syncthreads();
+        tail = true;
+        const uint32_t nd = d + (W >= 16 ? 2u : 1u);  // digits shared by a bucket's keys
+        for (uint32_t e = warp; e < nbig; e += LB / 32) {
+          const uint2 en = big[e];
+          if (!(en.x >> 31)) continue;
+          const uint32_t s0 = en.y & 0xffffu, c = en.y >> 16;
+          if (c <= TINY_MAX) {
+            warp_tail_sort<R, K>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc);
           } else {
-            warp_copy<R>(stage + (size_t)o0 * R, out + (size_t)o0 * R, len, lane);
+            warp_copy<R>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, lane);
             if (lane == 0) {
-              Seg ns = {sg.off + o0, len, (uint8_t)d1, SRC_REC, MODE_NONE, 0, 0};
+              Seg ns = {sg.off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
               local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
-              atomicMax(&ctl->max_local_len[nxt], len);
+              atomicMax(&ctl->max_local_len[nxt], c);
             }
           }
         }
       }
     }
     done += n;
-    RS_PROF(3);
     __syncthreads();
-    RS_PROF(4);
-    if (tid < RADIX) cnt[tid] = 0;
-    if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-    if (tid == 0) { nbig = 0; nsml = 0; sh_d = 0; }
+    zero_cnt(tail ? cnt_bytes : (2u << W));
+    if (tid == 0) { s_nbig = 0; s_const = 0; }
     if (nb >= nlist) break;
     bi = nb;
     sg = nsg;
   }
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
-#ifdef RADSORT_PHASE_PROF
-  if (tid == 0) {
-    for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[8 + q], pf[q]);
-  }
-#endif
-#undef RS_PROF
 }
-
 // -------------------------------------------------------------- k_bounds
 // Multi-GPU splitter search: for probe m, the number of keys < probe (lt) and
 // <= probe (le) inside the SORTED record range [lo[m], hi[m]) of buf (binary

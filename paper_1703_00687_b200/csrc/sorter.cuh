@@ -8,26 +8,32 @@ namespace radsort {
 template <int R, int K>
 struct Sorter {
   static constexpr uint32_t C = local_capacity<R>();
-  static constexpr int LOCAL_SCRATCH = (LOCAL_B / 32) * (int)sizeof(TailScratch<K>);
-  static constexpr int LOCAL_DYN_MAX = LOCAL_SMEM_BYTES + LOCAL_SCRATCH + 16384;
   static constexpr int CHILD_SCRATCH = (CHILD_B / 32) * (int)TINY_MAX * R;
+  static constexpr size_t LOCAL_SMEM_MAX = 227 * 1024 - 1024;  // dynamic smem ceiling per CTA (static smem aside)
 
   template <int IL, int LB>
-  static void launch_local_t(uint32_t nloc, size_t stage_bytes, const Seg* list, Seg* next, int nxt, Ctl* ctl,
+  static void launch_local_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                              uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
-    // 32-bit enumeration-sort keys for small bins (two CTAs per SM still fit)
-    const size_t sk_bytes = stage_bytes <= 65536 ? ((stage_bytes / R + 8) * 4 + 15) & ~(size_t)15 : 0;
-    const size_t smem = stage_bytes + (LB / 32) * sizeof(TailScratch<K>) + sk_bytes;
+    // smem: staged bin | 2^W u16 counters (aliased by the tail sorter's per-warp
+    // scratch) | list of buckets with > ES_MAX records
+    const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
+    const size_t tail_bytes = (LB / 32) * sizeof(TailScratch<K>);
+    const size_t big_bytes = (((size_t)maxlen / (es_max<R>() + 1) + 2) * 8 + 15) & ~(size_t)15;
+    uint32_t wmax = local_width(maxlen, 16);
+    auto cnt_of = [&](uint32_t w) { return std::max((size_t)2 << w, tail_bytes); };
+    while (wmax > LOCAL_WMIN && stage_bytes + cnt_of(wmax) + big_bytes > LOCAL_SMEM_MAX) --wmax;
+    const size_t cnt_bytes = cnt_of(wmax);
+    const size_t smem = stage_bytes + cnt_bytes + big_bytes;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_local<R, K, IL, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, LOCAL_DYN_MAX);
+      cudaFuncSetAttribute(k_local<R, K, IL, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOCAL_SMEM_MAX);
       attr = true;
     }
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
-    k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, (uint32_t)stage_bytes, (uint32_t)sk_bytes, next, nxt, ctl,
-                                               recs, tmp);
+    k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, next, nxt,
+                                               ctl, recs, tmp);
   }
 
   static void set_attrs() {
@@ -37,19 +43,25 @@ struct Sorter {
     done = true;
   }
 
-  // Local bins of up to `maxlen` records: IL = records per thread.
+  // Local bins of up to `maxlen` records: IL records per thread, at most 256
+  // bytes of records per thread; 256-thread CTAs (two per SM) unless the bins
+  // need 512 threads.
   static void launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                            uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
-    const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
-    const uint32_t il = (maxlen + LOCAL_B - 1) / LOCAL_B;
-#define RS_LOCAL(IL) launch_local_t<IL, LOCAL_B>(nloc, stage_bytes, list, next, nxt, ctl, recs, tmp, st, sms)
+    constexpr int ILMAX = 256 / R;
+    if ((size_t)maxlen > (size_t)256 * ILMAX) {
+      launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms);
+      return;
+    }
+    const uint32_t il = (maxlen + 255) / 256;
+#define RS_LOCAL(IL) launch_local_t<IL, 256>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms)
     if (il <= 1) RS_LOCAL(1);
     else if (il <= 2) RS_LOCAL(2);
     else if (il <= 4) RS_LOCAL(4);
     else if (il <= 8) RS_LOCAL(8);
-    else if constexpr (R <= 16) {
+    else if constexpr (ILMAX >= 16) {
       if (il <= 16) RS_LOCAL(16);
-      else if constexpr (R <= 8) RS_LOCAL(32);
+      else if constexpr (ILMAX >= 32) RS_LOCAL(32);
     }
 #undef RS_LOCAL
   }
