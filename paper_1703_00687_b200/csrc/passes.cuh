@@ -659,25 +659,25 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
 //
 // Per bin, with the bin's records in registers:
 //  1. counting pass on a composite digit of W bits -- digit d followed by the
-//     leading W-8 bits of digit d+1 (W = log2(bin)+1, 10..16; DESIGN.md §4:
-//     one smem counting pass that does the work of up to two MSD levels) --
-//     u16 counters, two per word, ranks from smem atomics;
+//     leading W-8 bits of digit d+1 (W = ceil(log2(bin)), 10..16; DESIGN.md §4:
+//     one smem counting pass doing the work of up to two MSD levels) -- u16
+//     counters, two per word, ranks from smem atomics;
+//     The record that finds one earlier record in its bucket lists the bucket
+//     (a dense list of the buckets holding >= 2 records).  A bucket holding
+//     the whole bin means constant leading digits: the AND/OR of the keys
+//     picks the first non-constant digit and the pass is redone
+//     there, or the bin is final when all keys are equal;
 //  2. exclusive scan of the counters (warp-cooperative, 16-byte accesses);
-//     a bucket holding the whole bin means constant leading digits: the AND/OR
-//     of the keys picks the first non-constant digit and the pass
-//     is redone there, or the bin is final when all keys are equal;
 //  3. every record is stored to smem at its bucket position, and the next
 //     bin's loads are issued right away (registers are free again);
-//  4. write-out, one coalesced pass over the staged bin: a record alone in its
-//     bucket is final; the records of a bucket of 2..ES_MAX get their place by
-//     enumeration sort on the full key among that bucket only (PAPER.md:102-104
-//     ES; ties by staged position); a larger bucket holding a single key is
-//     final as staged ("bins with all keys equal");
-//  5. larger buckets holding several keys (only duplicated or skewed keys
+//  4. one thread per listed bucket of 2..ES_MAX records sorts it in place in
+//     smem (insertion sort on the full key, PAPER.md:94 / PAPER.md:177: the
+//     fix-up sorter for a handful of records); a larger bucket is checked by a
+//     warp for holding a single key (final as staged);
+//  5. the staged bin is written out with coalesced stores;
+//  6. larger buckets holding several keys (only duplicated or skewed keys
 //     produce them): <= TINY_MAX records by the warp tail sorter, larger ones
-//     are written out and queued as Local bins of the next level.
-// Writes stay coalesced: a warp writes 32 consecutive staged records, each
-// to a place inside its own (small) bucket.
+//     are queued as Local bins of the next level.
 constexpr uint32_t LOCAL_WMIN = 10;  // narrowest composite digit: 2^(W-1) >= 512 counter words
 
 // Bucket of a key at depth d (< K): the top W bits of the key bits below its
@@ -696,19 +696,16 @@ __device__ __forceinline__ uint32_t bucket_of(const Key<16>& k, uint32_t d, uint
 
 __host__ __device__ __forceinline__ uint32_t local_width(uint32_t n, uint32_t wmax) {
   uint32_t w = 1;
-  while ((1u << w) < n) ++w;  // ceil(log2 n)
-  w += 1;
+  while ((1u << w) < n) ++w;  // ceil(log2 n): about one record per bucket
   return w < LOCAL_WMIN ? LOCAL_WMIN : (w > wmax ? wmax : w);
 }
 
 // In-place exclusive scan of the 2^W u16 bucket counters (two per word): one
-// contiguous chunk per warp, 16-byte accesses.  Buckets with more than `es`
-// records are appended to `big` as {bucket, start | count << 16}; *s_const is
-// set when a bucket holds all n records.  Contains one block barrier; the
-// caller synchronises after it.
+// contiguous chunk per warp, 16-byte accesses, the two halves of a word summed
+// as one 32-bit add (no half overflows: every count and sum is <= n <= 2^14).
+// Contains one block barrier; the caller synchronises after it.
 template <int LB>
-__device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t n, uint32_t es, uint2* big,
-                                           uint32_t* s_nbig, uint32_t* s_const, uint32_t* wsum) {
+__device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* wsum) {
   constexpr int NW = LB / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t pw = (1u << (W - 1)) / NW;  // words per warp, a multiple of 4
@@ -717,10 +714,9 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t n
   uint32_t tot = 0;
   for (uint32_t j = lane; j < n4; j += 32) {
     const uint4 v = c4[j];
-    tot += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) + (v.z & 0xffffu) + (v.z >> 16) +
-           (v.w & 0xffffu) + (v.w >> 16);
+    tot += v.x + v.y + v.z + v.w;
   }
-  tot = __reduce_add_sync(0xffffffffu, tot);
+  tot = __reduce_add_sync(0xffffffffu, (tot & 0xffffu) + (tot >> 16));
   if (lane == 0) wsum[warp] = tot;
   __syncthreads();
   uint32_t carry = 0;
@@ -729,37 +725,22 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t n
   for (uint32_t j0 = 0; j0 < n4; j0 += 32) {
     const uint32_t j = j0 + lane;
     const uint4 v = j < n4 ? c4[j] : make_uint4(0, 0, 0, 0);
-    const uint32_t c[8] = {v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16,
-                           v.z & 0xffffu, v.z >> 16, v.w & 0xffffu, v.w >> 16};
-    uint32_t t = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += c[k];
+    const uint32_t p = v.x + v.y + v.z + v.w;
+    const uint32_t t = (p & 0xffffu) + (p >> 16);
     uint32_t inc = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += y;
     }
+    // word start (both halves) = s | s << 16, then + (lo << 16) for the high half
     uint32_t s = carry + inc - t;
-    uint32_t st[8];
-    bool any_big = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      st[k] = s;
-      s += c[k];
-      any_big |= c[k] > es;
-    }
-    if (any_big) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (c[k] > es) {
-          if (c[k] == n) *s_const = 1u;
-          const uint32_t b = 2u * (warp * pw + 4u * j) + (uint32_t)k;
-          big[atomicAdd(s_nbig, 1u)] = make_uint2(b, st[k] | (c[k] << 16));
-        }
-      }
-    }
-    if (j < n4) c4[j] = make_uint4(st[0] | (st[1] << 16), st[2] | (st[3] << 16), st[4] | (st[5] << 16), st[6] | (st[7] << 16));
+    uint4 o4;
+    o4.x = s * 0x10001u + (v.x << 16); s += (v.x & 0xffffu) + (v.x >> 16);
+    o4.y = s * 0x10001u + (v.y << 16); s += (v.y & 0xffffu) + (v.y >> 16);
+    o4.z = s * 0x10001u + (v.z << 16); s += (v.z & 0xffffu) + (v.z >> 16);
+    o4.w = s * 0x10001u + (v.w << 16);
+    if (j < n4) c4[j] = o4;
     carry += __shfl_sync(0xffffffffu, inc, 31);
   }
 }
@@ -767,17 +748,18 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t n
 template <int R, int K, int IL, int LB>
 __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes, uint32_t cnt_bytes,
-            Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
+            uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
   extern __shared__ uint4 smem_raw[];
   constexpr int KW = K / 8;
+  constexpr int NW = LB / 32;
   constexpr uint32_t ES = es_max<R>();
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + stage_bytes);              // 2^W u16 counters
-  uint2* big = reinterpret_cast<uint2*>(stage + stage_bytes + cnt_bytes);        // buckets of > ES records
-  __shared__ uint32_t wsum[LB / 32], s_nbig, s_const;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + stage_bytes);                 // 2^W u16 counters
+  uint32_t* blist = reinterpret_cast<uint32_t*>(stage + stage_bytes + cnt_bytes);   // buckets of >= 2 records
+  __shared__ uint32_t wsum[NW], s_ncol, s_nbig, s_const;
   __shared__ unsigned long long sna[2], so[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(cnt)[warp];  // aliases cnt in phase 5 only
+  TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(cnt)[warp];  // aliases cnt in step 6 only
   uint32_t bi = blockIdx.x;
   if (bi >= nlist) return;
   auto zero_cnt = [&](uint32_t bytes) {
@@ -786,12 +768,11 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
   };
   Rec<R> r[IL];
   auto load = [&](const Seg& g) {
-    const uint8_t* src = buf_of(g.src, recs, tmp) + (size_t)g.off * R;
+    const uint8_t* p = buf_of(g.src, recs, tmp) + ((size_t)g.off + tid) * R;
+    const int lim = (int)g.len - tid;
 #pragma unroll
-    for (int i = 0; i < IL; ++i) {
-      const uint32_t idx = (uint32_t)(i * LB + tid);
-      if (idx < g.len) r[i] = ldg_rec<R>(src + (size_t)idx * R);
-    }
+    for (int i = 0; i < IL; ++i)
+      if (i * LB < lim) r[i] = ldg_rec<R>(p + (size_t)i * LB * R);
   };
   auto prefetch_l2 = [&](uint32_t b) {  // TMA bulk prefetch of a whole bin into L2
     if (tid == 0 && b < nlist) {
@@ -808,40 +789,48 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
   prefetch_l2(bi + gridDim.x);
   zero_cnt(cnt_bytes);
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-  if (tid == 0) { s_nbig = 0; s_const = 0; }
+  if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
   unsigned long long done = 0;
   constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
   for (;;) {
     const uint32_t n = sg.len;
+    const int lim = (int)n - tid;
     uint8_t* out = recs + (size_t)sg.off * R;
     uint32_t d = sg.depth;
-    uint32_t W = local_width(n, wmax);
+    const uint32_t W = local_width(n, wmax);
+    const uint32_t nbk = 1u << W;
     uint32_t rk[IP];
+    uint32_t ones = 0;
     bool all_equal = false;
     __syncthreads();  // counters zero, flags reset
     for (;;) {  // one round unless the composite digit is constant over the bin
 #pragma unroll
       for (int i = 0; i < IP; ++i) rk[i] = 0;
+      ones = 0;
+      bool cst = false;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LB + tid);
-        if (idx < n) {
+        if (i * LB < lim) {
           const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
           const uint32_t sh = 16u * (b & 1u);
-          const uint32_t old = atomicAdd(&cnt[b >> 1], 1u << sh);
-          rk[i >> 1] |= ((old >> sh) & 0xffffu) << (16 * (i & 1));
+          const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
+          rk[i >> 1] |= old << (16 * (i & 1));
+          ones += (uint32_t)(old == 1u);  // the second record of a bucket will list it
+          cst |= old == n - 1u;           // the whole bin in one bucket
         }
       }
+      if (cst) s_const = 1u;
       __syncthreads();
-      local_scan<LB>(cnt, W, n, ES, big, &s_nbig, &s_const, wsum);
-      __syncthreads();
-      if (!s_const) break;
+      if (!s_const) {
+        local_scan<LB>(cnt, W, wsum);
+        __syncthreads();
+        break;
+      }
       // every record in one bucket: skip the constant digits
       uint64_t na[2] = {0, 0}, o[2] = {0, 0};
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LB + tid);
-        if (idx < n) {
+        if (i * LB < lim) {
           const Key<K> k = key_of<R, K>(r[i]);
           na[0] |= ~k.w0; o[0] |= k.w0;
           if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
@@ -861,27 +850,37 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
       __syncthreads();
       zero_cnt(2u << W);
       if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
-      if (tid == 0) { s_nbig = 0; s_const = 0; }
+      if (tid == 0) s_const = 0;
       __syncthreads();
       if (d2 >= (uint32_t)K) { all_equal = true; break; }
       d = d2;
     }
+    const uint16_t* start16 = reinterpret_cast<const uint16_t*>(cnt);
+    auto start_of = [&](uint32_t b) { return (uint32_t)start16[b]; };
     if (all_equal) {  // final where it is (copied out of tmp)
       if (sg.src == SRC_TMP) {
 #pragma unroll
-        for (int i = 0; i < IL; ++i) {
-          const uint32_t idx = (uint32_t)(i * LB + tid);
-          if (idx < n) st_rec<R>(out + (size_t)idx * R, r[i]);
-        }
+        for (int i = 0; i < IL; ++i)
+          if (i * LB < lim) st_rec<R>(out + (size_t)(i * LB + tid) * R, r[i]);
       }
     } else {
+      // slots in the list of buckets holding >= 2 records: warp scan + one atomic per warp
+      uint32_t inc = ones;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      uint32_t slot = 0;
+      if (lane == 31 && inc) slot = atomicAdd(&s_ncol, inc);
+      slot = __shfl_sync(0xffffffffu, slot, 31) + inc - ones;
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
-        const uint32_t idx = (uint32_t)(i * LB + tid);
-        if (idx < n) {
+        if (i * LB < lim) {
           const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
-          const uint32_t s = (cnt[b >> 1] >> (16u * (b & 1u))) & 0x7fffu;
-          st_rec<R>(stage + (size_t)(s + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)) * R, r[i]);
+          const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+          st_rec<R>(stage + (size_t)(start_of(b) + rnk) * R, r[i]);
+          if (rnk == 1u) blist[slot++] = b;
         }
       }
     }
@@ -896,65 +895,51 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     prefetch_l2(nb + gridDim.x);
     bool tail = false;
     if (!all_equal) {
-      const uint32_t nbk = 1u << W;
-      const int rem = 8 * ((int)K - (int)d) - (int)W;  // key bits below the composite digit
-      auto start_of = [&](uint32_t b) { return (cnt[b >> 1] >> (16u * (b & 1u))) & 0xffffu; };
-      const uint32_t nbig = s_nbig;
-      __syncthreads();
-      if (nbig && rem > 0) {  // flag the big buckets that hold more than one key
-        for (uint32_t q = tid; q < n; q += LB) {
-          const Key<K> kx = ld_key<R, K>(stage + (size_t)q * R);
-          const uint32_t b = bucket_of(kx, d, W);
-          const uint32_t s0 = start_of(b) & 0x7fffu, s1 = b + 1 < nbk ? start_of(b + 1) & 0x7fffu : n;
-          if (s1 - s0 > ES && !key_eq(ld_key<R, K>(stage + (size_t)s0 * R), kx))
-            atomicOr(&cnt[b >> 1], 0x8000u << (16u * (b & 1u)));
-        }
-        __syncthreads();
-      }
-      for (uint32_t q = tid; q < n; q += LB) {
-        const Rec<R> x = ld_rec<R>(stage + (size_t)q * R);
-        uint32_t dest = q;
-        if (rem > 0) {
-          const Key<K> kx = key_of<R, K>(x);
-          const uint32_t b = bucket_of(kx, d, W);
-          const uint32_t w0 = start_of(b);
-          const uint32_t s0 = w0 & 0x7fffu, s1 = b + 1 < nbk ? start_of(b + 1) & 0x7fffu : n;
-          const uint32_t c = s1 - s0;
-          if (c > ES) {
-            if (w0 & 0x8000u) continue;  // several keys: phase 5
-          } else if (c > 1) {            // enumeration sort inside the bucket
-            uint32_t rank = 0;
-            for (uint32_t j = s0; j < s1; ++j) {
-              const Key<K> kj = ld_key<R, K>(stage + (size_t)j * R);
-              rank += (uint32_t)key_lt(kj, kx) | ((uint32_t)(j < q) & (uint32_t)key_eq(kj, kx));
-            }
-            dest = s0 + rank;
+      const bool fix = 8 * ((int)K - (int)d) > (int)W;  // key bits left below the composite digit
+      __syncthreads();  // staged
+      const uint32_t ncol = s_ncol;
+      uint32_t nbig = 0;
+      if (fix && ncol) {
+        for (uint32_t e = tid; e < ncol; e += LB) {
+          const uint32_t b = blist[e];
+          const uint32_t s0 = start_of(b), c = (b + 1 < nbk ? start_of(b + 1) : n) - s0;
+          uint8_t* base = stage + (size_t)s0 * R;
+          if (c == 2) {  // a pair: one compare-exchange
+            const Rec<R> x = ld_rec<R>(base), y = ld_rec<R>(base + R);
+            if (key_lt(key_of<R, K>(y), key_of<R, K>(x))) { st_rec<R>(base, y); st_rec<R>(base + R, x); }
+          } else if (c <= ES) {  // 3..ES records: insertion sort in place
+            lane_insertion_sort<R, K>(base, c);
+          } else {  // more: listed from the top as {start | count << 16}
+            blist[cap - 1u - atomicAdd(&s_nbig, 1u)] = s0 | (c << 16);
           }
         }
-        st_rec<R>(out + (size_t)dest * R, x);
-      }
-      if (nbig && rem > 0) {
-        __syncthreads();  // counters no longer read: mark mixed big buckets, then reuse cnt as tail scratch
-        for (uint32_t e = tid; e < nbig; e += LB) {
-          const uint32_t b = big[e].x;
-          if (start_of(b) & 0x8000u) big[e].x = b | 0x80000000u;
-        }
         __syncthreads();
+        nbig = s_nbig;
+        for (uint32_t e = warp; e < nbig; e += NW) {  // > ES records: one key or several?
+          const uint32_t en = blist[cap - 1u - e];
+          const uint32_t s0 = en & 0xffffu, c = en >> 16;
+          const Key<K> k0 = ld_key<R, K>(stage + (size_t)s0 * R);
+          bool diff = false;
+          for (uint32_t j = s0 + lane; j < s0 + c; j += 32) diff |= !key_eq(ld_key<R, K>(stage + (size_t)j * R), k0);
+          if (__any_sync(0xffffffffu, diff) && lane == 0) blist[cap - 1u - e] = en | 0x80000000u;
+        }
+        if (nbig) __syncthreads();
+      }
+      for (uint32_t q = tid; q < n; q += LB) st_rec<R>(out + (size_t)q * R, ld_rec<R>(stage + (size_t)q * R));
+      if (nbig) {
+        __syncthreads();  // written out; counters dead: the tail sorter's scratch aliases them
         tail = true;
         const uint32_t nd = d + (W >= 16 ? 2u : 1u);  // digits shared by a bucket's keys
-        for (uint32_t e = warp; e < nbig; e += LB / 32) {
-          const uint2 en = big[e];
-          if (!(en.x >> 31)) continue;
-          const uint32_t s0 = en.y & 0xffffu, c = en.y >> 16;
+        for (uint32_t e = warp; e < nbig; e += NW) {
+          const uint32_t en = blist[cap - 1u - e];
+          if (!(en >> 31)) continue;
+          const uint32_t s0 = en & 0xffffu, c = (en >> 16) & 0x7fffu;
           if (c <= TINY_MAX) {
             warp_tail_sort<R, K>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc);
-          } else {
-            warp_copy<R>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, lane);
-            if (lane == 0) {
-              Seg ns = {sg.off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
-              local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
-              atomicMax(&ctl->max_local_len[nxt], c);
-            }
+          } else if (lane == 0) {
+            Seg ns = {sg.off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
+            local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
+            atomicMax(&ctl->max_local_len[nxt], c);
           }
         }
       }
@@ -962,13 +947,14 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     done += n;
     __syncthreads();
     zero_cnt(tail ? cnt_bytes : (2u << W));
-    if (tid == 0) { s_nbig = 0; s_const = 0; }
+    if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
     if (nb >= nlist) break;
     bi = nb;
     sg = nsg;
   }
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
 }
+
 // -------------------------------------------------------------- k_bounds
 // Multi-GPU splitter search: for probe m, the number of keys < probe (lt) and
 // <= probe (le) inside the SORTED record range [lo[m], hi[m]) of buf (binary

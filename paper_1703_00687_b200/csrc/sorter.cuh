@@ -15,10 +15,11 @@ struct Sorter {
   static void launch_local_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                              uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
     // smem: staged bin | 2^W u16 counters (aliased by the tail sorter's per-warp
-    // scratch) | list of buckets with > ES_MAX records
+    // scratch) | list of the buckets holding >= 2 records
     const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
     const size_t tail_bytes = (LB / 32) * sizeof(TailScratch<K>);
-    const size_t big_bytes = (((size_t)maxlen / (es_max<R>() + 1) + 2) * 8 + 15) & ~(size_t)15;
+    const uint32_t cap = maxlen / 2 + 1;  // buckets holding >= 2 records
+    const size_t big_bytes = ((size_t)cap * 4 + 15) & ~(size_t)15;
     uint32_t wmax = local_width(maxlen, 16);
     auto cnt_of = [&](uint32_t w) { return std::max((size_t)2 << w, tail_bytes); };
     while (wmax > LOCAL_WMIN && stage_bytes + cnt_of(wmax) + big_bytes > LOCAL_SMEM_MAX) --wmax;
@@ -32,7 +33,7 @@ struct Sorter {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
-    k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, next, nxt,
+    k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt,
                                                ctl, recs, tmp);
   }
 
