@@ -695,8 +695,12 @@ __device__ __forceinline__ uint32_t bucket_of(const Key<16>& k, uint32_t d, uint
 }
 
 __host__ __device__ __forceinline__ uint32_t local_width(uint32_t n, uint32_t wmax) {
+#ifdef __CUDA_ARCH__
+  const uint32_t w = n > 1 ? 32u - (uint32_t)__clz((int)(n - 1)) : 1u;  // ceil(log2 n): about one record per bucket
+#else
   uint32_t w = 1;
-  while ((1u << w) < n) ++w;  // ceil(log2 n): about one record per bucket
+  while ((1u << w) < n) ++w;
+#endif
   return w < LOCAL_WMIN ? LOCAL_WMIN : (w > wmax ? wmax : w);
 }
 
@@ -719,9 +723,9 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* 
   tot = __reduce_add_sync(0xffffffffu, (tot & 0xffffu) + (tot >> 16));
   if (lane == 0) wsum[warp] = tot;
   __syncthreads();
-  uint32_t carry = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) carry += (w < warp) ? wsum[w] : 0u;
+  // carry-in of this warp's chunk: exclusive prefix of the warp totals (lane w holds warp w's)
+  uint32_t carry = (lane < NW && lane < warp) ? wsum[lane] : 0u;
+  carry = __reduce_add_sync(0xffffffffu, carry);
   for (uint32_t j0 = 0; j0 < n4; j0 += 32) {
     const uint32_t j = j0 + lane;
     const uint4 v = j < n4 ? c4[j] : make_uint4(0, 0, 0, 0);
@@ -745,6 +749,64 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* 
   }
 }
 
+// Steps 4-6 of the CTA-local sort, for a bin staged in smem in bucket order
+// (see k_local).  All threads of the CTA call it (it contains barriers).
+// Returns true when the tail sorter used the counter region as scratch.
+template <int R, int K, int LB, int NTW>
+__device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* start16, uint32_t* blist, uint32_t cap,
+                                             uint32_t n, uint32_t nbk, uint32_t d, uint32_t W, uint32_t ncol,
+                                             uint32_t* s_nbig, TailScratch<K>* tsc, uint8_t* out, uint32_t off,
+                                             Seg* local_next, int nxt, Ctl* ctl) {
+  constexpr int NW = LB / 32;
+  constexpr uint32_t ES = es_max<R>();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto start_of = [&](uint32_t b) { return (uint32_t)start16[b]; };
+  uint32_t nbig = 0;
+  if (ncol) {
+    for (uint32_t e = tid; e < ncol; e += LB) {
+      const uint32_t b = blist[e];
+      const uint32_t s0 = start_of(b), c = (b + 1 < nbk ? start_of(b + 1) : n) - s0;
+      uint8_t* base = stage + (size_t)s0 * R;
+      if (c == 2) {  // a pair: one compare-exchange
+        const Rec<R> x = ld_rec<R>(base), y = ld_rec<R>(base + R);
+        if (key_lt(key_of<R, K>(y), key_of<R, K>(x))) { st_rec<R>(base, y); st_rec<R>(base + R, x); }
+      } else if (c <= ES) {  // 3..ES records: insertion sort in place
+        lane_insertion_sort<R, K>(base, c);
+      } else {  // more: listed from the top as {start | count << 16}
+        blist[cap - 1u - atomicAdd(s_nbig, 1u)] = s0 | (c << 16);
+      }
+    }
+    __syncthreads();
+    nbig = *s_nbig;
+    for (uint32_t e = warp; e < nbig; e += NW) {  // > ES records: one key or several?
+      const uint32_t en = blist[cap - 1u - e];
+      const uint32_t s0 = en & 0xffffu, c = en >> 16;
+      const Key<K> k0 = ld_key<R, K>(stage + (size_t)s0 * R);
+      bool diff = false;
+      for (uint32_t j = s0 + lane; j < s0 + c; j += 32) diff |= !key_eq(ld_key<R, K>(stage + (size_t)j * R), k0);
+      if (__any_sync(0xffffffffu, diff) && lane == 0) blist[cap - 1u - e] = en | 0x80000000u;
+    }
+    if (nbig) __syncthreads();
+  }
+  for (uint32_t q = tid; q < n; q += LB) st_rec<R>(out + (size_t)q * R, ld_rec<R>(stage + (size_t)q * R));
+  if (!nbig) return false;
+  __syncthreads();  // written out; counters dead: the tail sorter's scratch aliases them
+  const uint32_t nd = d + (W >= 16 ? 2u : 1u);  // digits shared by a bucket's keys
+  for (uint32_t e = warp; e < nbig && warp < NTW; e += NTW) {
+    const uint32_t en = blist[cap - 1u - e];
+    if (!(en >> 31)) continue;
+    const uint32_t s0 = en & 0xffffu, c = (en >> 16) & 0x7fffu;
+    if (c <= TINY_MAX) {
+      warp_tail_sort<R, K>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc[warp]);
+    } else if (lane == 0) {
+      Seg ns = {off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
+      local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
+      atomicMax(&ctl->max_local_len[nxt], c);
+    }
+  }
+  return true;
+}
+
 template <int R, int K, int IL, int LB>
 __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes, uint32_t cnt_bytes,
@@ -759,7 +821,6 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
   __shared__ uint32_t wsum[NW], s_ncol, s_nbig, s_const;
   __shared__ unsigned long long sna[2], so[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  TailScratch<K>& tsc = reinterpret_cast<TailScratch<K>*>(cnt)[warp];  // aliases cnt in step 6 only
   uint32_t bi = blockIdx.x;
   if (bi >= nlist) return;
   auto zero_cnt = [&](uint32_t bytes) {
@@ -791,6 +852,12 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
   if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
   unsigned long long done = 0;
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = clock64(), tB = 0;
+#define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
+#else
+#define RS_PROF(i) do { } while (0)
+#endif
   constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
   for (;;) {
     const uint32_t n = sg.len;
@@ -803,6 +870,7 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     uint32_t ones = 0;
     bool all_equal = false;
     __syncthreads();  // counters zero, flags reset
+    RS_PROF(7);
     for (;;) {  // one round unless the composite digit is constant over the bin
 #pragma unroll
       for (int i = 0; i < IP; ++i) rk[i] = 0;
@@ -821,9 +889,11 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
       }
       if (cst) s_const = 1u;
       __syncthreads();
+      RS_PROF(0);
       if (!s_const) {
         local_scan<LB>(cnt, W, wsum);
         __syncthreads();
+        RS_PROF(1);
         break;
       }
       // every record in one bucket: skip the constant digits
@@ -896,56 +966,15 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     bool tail = false;
     if (!all_equal) {
       const bool fix = 8 * ((int)K - (int)d) > (int)W;  // key bits left below the composite digit
+      RS_PROF(2);
       __syncthreads();  // staged
-      const uint32_t ncol = s_ncol;
-      uint32_t nbig = 0;
-      if (fix && ncol) {
-        for (uint32_t e = tid; e < ncol; e += LB) {
-          const uint32_t b = blist[e];
-          const uint32_t s0 = start_of(b), c = (b + 1 < nbk ? start_of(b + 1) : n) - s0;
-          uint8_t* base = stage + (size_t)s0 * R;
-          if (c == 2) {  // a pair: one compare-exchange
-            const Rec<R> x = ld_rec<R>(base), y = ld_rec<R>(base + R);
-            if (key_lt(key_of<R, K>(y), key_of<R, K>(x))) { st_rec<R>(base, y); st_rec<R>(base + R, x); }
-          } else if (c <= ES) {  // 3..ES records: insertion sort in place
-            lane_insertion_sort<R, K>(base, c);
-          } else {  // more: listed from the top as {start | count << 16}
-            blist[cap - 1u - atomicAdd(&s_nbig, 1u)] = s0 | (c << 16);
-          }
-        }
-        __syncthreads();
-        nbig = s_nbig;
-        for (uint32_t e = warp; e < nbig; e += NW) {  // > ES records: one key or several?
-          const uint32_t en = blist[cap - 1u - e];
-          const uint32_t s0 = en & 0xffffu, c = en >> 16;
-          const Key<K> k0 = ld_key<R, K>(stage + (size_t)s0 * R);
-          bool diff = false;
-          for (uint32_t j = s0 + lane; j < s0 + c; j += 32) diff |= !key_eq(ld_key<R, K>(stage + (size_t)j * R), k0);
-          if (__any_sync(0xffffffffu, diff) && lane == 0) blist[cap - 1u - e] = en | 0x80000000u;
-        }
-        if (nbig) __syncthreads();
-      }
-      for (uint32_t q = tid; q < n; q += LB) st_rec<R>(out + (size_t)q * R, ld_rec<R>(stage + (size_t)q * R));
-      if (nbig) {
-        __syncthreads();  // written out; counters dead: the tail sorter's scratch aliases them
-        tail = true;
-        const uint32_t nd = d + (W >= 16 ? 2u : 1u);  // digits shared by a bucket's keys
-        for (uint32_t e = warp; e < nbig; e += NW) {
-          const uint32_t en = blist[cap - 1u - e];
-          if (!(en >> 31)) continue;
-          const uint32_t s0 = en & 0xffffu, c = (en >> 16) & 0x7fffu;
-          if (c <= TINY_MAX) {
-            warp_tail_sort<R, K>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc);
-          } else if (lane == 0) {
-            Seg ns = {sg.off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
-            local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
-            atomicMax(&ctl->max_local_len[nxt], c);
-          }
-        }
-      }
+      RS_PROF(3);
+      tail = local_finish<R, K, LB, NW>(stage, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
+                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl);
     }
     done += n;
     __syncthreads();
+    RS_PROF(5);
     zero_cnt(tail ? cnt_bytes : (2u << W));
     if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
     if (nb >= nlist) break;
@@ -953,6 +982,12 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     sg = nsg;
   }
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
+#ifdef RADSORT_PHASE_PROF
+  if (tid == 0) {
+    for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[8 + q], pf[q]);
+  }
+#endif
+#undef RS_PROF
 }
 
 // -------------------------------------------------------------- k_bounds
