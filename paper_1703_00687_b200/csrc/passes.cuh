@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
 //
 // Per bin, with the bin's records in registers:
 //  1. counting pass on a composite digit of W bits -- digit d followed by the
-//     leading W-8 bits of digit d+1 (W = ceil(log2(bin)), 10..16; DESIGN.md §4:
+//     leading W-8 bits of digit d+1 (W = ceil(log2(bin)) + 1, 10..16; DESIGN.md §4:
 //     one smem counting pass doing the work of up to two MSD levels) -- u16
 //     counters, two per word, ranks from smem atomics;
 //     The record that finds one earlier record in its bucket lists the bucket
@@ -695,11 +695,13 @@ __device__ __forceinline__ uint32_t bucket_of(const Key<16>& k, uint32_t d, uint
 }
 
 __host__ __device__ __forceinline__ uint32_t local_width(uint32_t n, uint32_t wmax) {
+  // ceil(log2 n) + 1: about half a record per bucket (measured best)
 #ifdef __CUDA_ARCH__
-  const uint32_t w = n > 1 ? 32u - (uint32_t)__clz((int)(n - 1)) : 1u;  // ceil(log2 n): about one record per bucket
+  const uint32_t w = (n > 1 ? 32u - (uint32_t)__clz((int)(n - 1)) : 1u) + 1u;
 #else
   uint32_t w = 1;
   while ((1u << w) < n) ++w;
+  ++w;
 #endif
   return w < LOCAL_WMIN ? LOCAL_WMIN : (w > wmax ? wmax : w);
 }
