@@ -451,11 +451,11 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     if (sg.mode == MODE_SCATTER) {
       const uint32_t d = sg.depth;
       uint32_t pre_excl = 0;
-      if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry), loaded early
+      if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry) + bin base, loaded early
         if (tid < RADIX) {
           const uint32_t per = (total + hist_grid - 1) / hist_grid;
           const uint32_t ch = t / per;
-          pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) +
+          pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
                      (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
         }
       }
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       if (tid < RADIX) {
         uint64_t excl = 0;
         if constexpr (PRE) {
-          excl = pre_excl;
+          excl = pre_excl;  // includes the bin base
         } else if (lt > 0) {
           // windowed decoupled look-back over this segment's earlier tiles
           uint32_t p = t - 1;
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
           }
           st_relaxed(my, ep | ST_PREFIX | (excl + c));
         }
-        gofs[tid] = segbase[(size_t)s * RADIX + tid] + (uint32_t)excl - ex;
+        gofs[tid] = (PRE ? 0u : segbase[(size_t)s * RADIX + tid]) + (uint32_t)excl - ex;
       }
       __syncthreads();
       RS_PROF(4);
