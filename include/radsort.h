@@ -90,7 +90,11 @@ radsort_status radsort_init(int device);
  *                permuted so keys are non-decreasing.
  *   dev_tmp      scratch of >= n*rec_size bytes, 16-byte aligned, must not
  *                overlap dev_records; contents undefined afterwards.
- *   rec_size     8, 16 or 32 (built layouts; 24/40/48/56/64 -> UNSUPPORTED).
+ *   rec_size     8, 16, 24, 32 or 40; built (rec_size, key_size) layouts:
+ *                (8,8) (16,8) (16,16) (24,8) (24,16) (32,8) (32,16) (40,16) --
+ *                SPEC.md:28-30's five paper layouts (8,0) (8,8) (8,16) (8,24)
+ *                (16,0) as (key+data, key) plus the 16-byte-key ones; other
+ *                multiples of 8 up to 64 -> RADSORT_ERR_UNSUPPORTED.
  *   key_size     8 or 16, key_size <= rec_size.
  *   stream       cudaStream_t (NULL = legacy default stream) on which all
  *                work is ordered.  The call blocks the host once per MSD level

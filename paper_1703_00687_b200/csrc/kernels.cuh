@@ -21,6 +21,8 @@ constexpr int CHILD_B = 256;           // threads per children CTA
 constexpr int LOCAL_SMEM_BYTES = 131072;  // CTA-local sorter capacity in bytes
 
 template <int R> __host__ __device__ constexpr uint32_t local_capacity() { return (uint32_t)(LOCAL_SMEM_BYTES / R); }
+// Records per scatter/histogram tile of TB bytes: a multiple of the scatter CTA size SB.
+template <int R, int TB, int SB> __host__ __device__ constexpr uint32_t tile_recs() { return (uint32_t)((TB / R) / SB * SB); }
 
 enum : uint8_t { SRC_REC = 0, SRC_TMP = 1 };
 enum : uint8_t { MODE_NONE = 0, MODE_SCATTER = 1, MODE_COPY = 2 };
@@ -57,12 +59,22 @@ template <int R> struct Rec;
 template <> struct Rec<8> { uint2 a; };
 template <> struct Rec<16> { uint4 a; };
 template <> struct Rec<32> { uint4 a, b; };
+template <> struct Rec<24> { uint2 a, b, c; };        // 8-byte aligned (SPEC.md:28-30 layouts (8,16), (16,8))
+template <> struct Rec<40> { uint2 a, b, c, d, e; };  // 8-byte aligned (layout (16,24))
 
 template <int R> __device__ __forceinline__ Rec<R> ld_rec(const uint8_t* p);
 template <> __device__ __forceinline__ Rec<8> ld_rec<8>(const uint8_t* p) { return {*reinterpret_cast<const uint2*>(p)}; }
 template <> __device__ __forceinline__ Rec<16> ld_rec<16>(const uint8_t* p) { return {*reinterpret_cast<const uint4*>(p)}; }
 template <> __device__ __forceinline__ Rec<32> ld_rec<32>(const uint8_t* p) {
   return {reinterpret_cast<const uint4*>(p)[0], reinterpret_cast<const uint4*>(p)[1]};
+}
+template <> __device__ __forceinline__ Rec<24> ld_rec<24>(const uint8_t* p) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+  return {q[0], q[1], q[2]};
+}
+template <> __device__ __forceinline__ Rec<40> ld_rec<40>(const uint8_t* p) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+  return {q[0], q[1], q[2], q[3], q[4]};
 }
 template <int R> __device__ __forceinline__ void st_rec(uint8_t* p, const Rec<R>& r);
 template <> __device__ __forceinline__ void st_rec<8>(uint8_t* p, const Rec<8>& r) { *reinterpret_cast<uint2*>(p) = r.a; }
@@ -71,12 +83,29 @@ template <> __device__ __forceinline__ void st_rec<32>(uint8_t* p, const Rec<32>
   reinterpret_cast<uint4*>(p)[0] = r.a;
   reinterpret_cast<uint4*>(p)[1] = r.b;
 }
+template <> __device__ __forceinline__ void st_rec<24>(uint8_t* p, const Rec<24>& r) {
+  uint2* q = reinterpret_cast<uint2*>(p);
+  q[0] = r.a; q[1] = r.b; q[2] = r.c;
+}
+template <> __device__ __forceinline__ void st_rec<40>(uint8_t* p, const Rec<40>& r) {
+  uint2* q = reinterpret_cast<uint2*>(p);
+  q[0] = r.a; q[1] = r.b; q[2] = r.c; q[3] = r.d; q[4] = r.e;
+}
 // read-only, non-coherent path for the streaming source of a pass
 template <int R> __device__ __forceinline__ Rec<R> ldg_rec(const uint8_t* p);
 template <> __device__ __forceinline__ Rec<8> ldg_rec<8>(const uint8_t* p) { return {__ldg(reinterpret_cast<const uint2*>(p))}; }
 template <> __device__ __forceinline__ Rec<16> ldg_rec<16>(const uint8_t* p) { return {__ldg(reinterpret_cast<const uint4*>(p))}; }
 template <> __device__ __forceinline__ Rec<32> ldg_rec<32>(const uint8_t* p) {
   return {__ldg(reinterpret_cast<const uint4*>(p)), __ldg(reinterpret_cast<const uint4*>(p) + 1)};
+}
+
+template <> __device__ __forceinline__ Rec<24> ldg_rec<24>(const uint8_t* p) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+  return {__ldg(q), __ldg(q + 1), __ldg(q + 2)};
+}
+template <> __device__ __forceinline__ Rec<40> ldg_rec<40>(const uint8_t* p) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+  return {__ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(q + 3), __ldg(q + 4)};
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return (uint64_t)lo | ((uint64_t)hi << 32); }
@@ -93,6 +122,9 @@ template <> __device__ __forceinline__ Key<8> key_of<16, 8>(const Rec<16>& r) { 
 template <> __device__ __forceinline__ Key<8> key_of<32, 8>(const Rec<32>& r) { return {u64of(r.a.x, r.a.y)}; }
 template <> __device__ __forceinline__ Key<16> key_of<16, 16>(const Rec<16>& r) { return {u64of(r.a.x, r.a.y), u64of(r.a.z, r.a.w)}; }
 template <> __device__ __forceinline__ Key<16> key_of<32, 16>(const Rec<32>& r) { return {u64of(r.a.x, r.a.y), u64of(r.a.z, r.a.w)}; }
+template <> __device__ __forceinline__ Key<8> key_of<24, 8>(const Rec<24>& r) { return {u64of(r.a.x, r.a.y)}; }
+template <> __device__ __forceinline__ Key<16> key_of<24, 16>(const Rec<24>& r) { return {u64of(r.a.x, r.a.y), u64of(r.b.x, r.b.y)}; }
+template <> __device__ __forceinline__ Key<16> key_of<40, 16>(const Rec<40>& r) { return {u64of(r.a.x, r.a.y), u64of(r.b.x, r.b.y)}; }
 
 // Digit d, d = 0 most significant ("1 B digits"): byte K-1-d.
 __device__ __forceinline__ uint32_t digit_of(const Key<8>& k, uint32_t d) {
@@ -331,6 +363,15 @@ template <> __device__ __forceinline__ Key<16> ld_key<16, 16>(const uint8_t* p) 
 template <> __device__ __forceinline__ Key<16> ld_key<32, 16>(const uint8_t* p) {
   const uint4 v = *reinterpret_cast<const uint4*>(p);
   return {u64of(v.x, v.y), u64of(v.z, v.w)};
+}
+template <> __device__ __forceinline__ Key<8> ld_key<24, 8>(const uint8_t* p) { return {*reinterpret_cast<const uint64_t*>(p)}; }
+template <> __device__ __forceinline__ Key<16> ld_key<24, 16>(const uint8_t* p) {
+  const uint64_t* q = reinterpret_cast<const uint64_t*>(p);
+  return {q[0], q[1]};
+}
+template <> __device__ __forceinline__ Key<16> ld_key<40, 16>(const uint8_t* p) {
+  const uint64_t* q = reinterpret_cast<const uint64_t*>(p);
+  return {q[0], q[1]};
 }
 __device__ __forceinline__ bool key_eq(const Key<8>& a, const Key<8>& b) { return a.w0 == b.w0; }
 __device__ __forceinline__ bool key_eq(const Key<16>& a, const Key<16>& b) { return (a.w0 == b.w0) & (a.w1 == b.w1); }

@@ -1,0 +1,12 @@
+// Instantiation of the radsort level loop and multi-GPU building blocks for
+// rec_size=24, key_size=16.
+#include "sorter.cuh"
+namespace radsort {
+template radsort_status run_layout<24, 16>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
+template radsort_status multi_hist<24, 16>(Context*, const uint8_t*, uint32_t, uint32_t, cudaStream_t, uint64_t*,
+                                           uint64_t*);
+template radsort_status multi_scatter<24, 16>(Context*, uint8_t*, uint8_t*, uint32_t, uint32_t, const uint64_t*,
+                                              cudaStream_t);
+template radsort_status multi_bounds<24, 16>(Context*, const uint8_t*, const uint32_t*, const uint32_t*,
+                                             const uint64_t*, uint32_t, cudaStream_t, uint64_t*, uint64_t*);
+}

@@ -119,12 +119,11 @@ static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint3
 // until the segment changes, so global atomics are per CTA and segment, not per
 // tile.  andor[s] = {OR of ~key words, OR of key words}: all accumulators start
 // at zero.
-template <int R, int K, int TB>
+template <int R, int K, uint32_t T>
 __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                  uint32_t nseg, const Ctl* __restrict__ ctl, uint32_t* __restrict__ hist,
                                                  unsigned long long* __restrict__ andor, const uint8_t* recs,
                                                  const uint8_t* tmp) {
-  constexpr uint32_t T = (uint32_t)(TB / R);
   constexpr int KW = K / 8;
   constexpr int U = 8;  // keys in flight per thread
   __shared__ uint32_t h[RADIX];
@@ -208,14 +207,13 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
 // and ch_tot[c][v] = count of digit v of the chunk's last segment in the chunk
 // (k_carry turns these into each chunk's carry-in).
 constexpr uint32_t NO_SEG = 0xffffffffu;
-template <int R, int K, int TB>
+template <int R, int K, uint32_t T>
 __global__ void __launch_bounds__(HIST_B) k_hist_pre(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                      uint32_t nseg, const Ctl* __restrict__ ctl,
                                                      uint32_t* __restrict__ hist, unsigned long long* __restrict__ andor,
                                                      const uint8_t* recs, const uint8_t* tmp, uint32_t* __restrict__ tile_pre,
                                                      uint32_t* __restrict__ ch_first, uint32_t* __restrict__ ch_last,
                                                      uint32_t* __restrict__ ch_tot) {
-  constexpr uint32_t T = (uint32_t)(TB / R);
   constexpr int KW = K / 8;
   constexpr int U = R <= 8 ? 16 : 8;  // keys in flight per thread
   __shared__ uint32_t h[RADIX], run[RADIX];
@@ -396,7 +394,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
                                                        uint8_t* recs, uint8_t* tmp, const uint32_t* __restrict__ tile_pre,
                                                        const uint32_t* __restrict__ ch_first,
                                                        const uint32_t* __restrict__ carry_in, uint32_t hist_grid) {
-  constexpr uint32_t T = (uint32_t)(TB / R);
+  constexpr uint32_t T = tile_recs<R, TB, SB>();
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
   extern __shared__ uint4 smem_raw[];

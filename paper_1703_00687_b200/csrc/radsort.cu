@@ -45,12 +45,18 @@ const LayoutOps* layout_ops(uint32_t R, uint32_t K) {
   RS_OPS(16, 16);
   RS_OPS(32, 8);
   RS_OPS(32, 16);
+  RS_OPS(24, 8);
+  RS_OPS(24, 16);
+  RS_OPS(40, 16);
 #undef RS_OPS
   if (R == 8 && K == 8) return &ops_8_8;
   if (R == 16 && K == 8) return &ops_16_8;
   if (R == 16 && K == 16) return &ops_16_16;
   if (R == 32 && K == 8) return &ops_32_8;
   if (R == 32 && K == 16) return &ops_32_16;
+  if (R == 24 && K == 8) return &ops_24_8;
+  if (R == 24 && K == 16) return &ops_24_16;
+  if (R == 40 && K == 16) return &ops_40_16;
   return nullptr;
 }
 
@@ -78,6 +84,9 @@ static radsort_status dispatch(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32
   if (R == 16 && K == 16) return run_layout<16, 16>(ctx, recs, tmp, n, st, s);
   if (R == 32 && K == 8) return run_layout<32, 8>(ctx, recs, tmp, n, st, s);
   if (R == 32 && K == 16) return run_layout<32, 16>(ctx, recs, tmp, n, st, s);
+  if (R == 24 && K == 8) return run_layout<24, 8>(ctx, recs, tmp, n, st, s);
+  if (R == 24 && K == 16) return run_layout<24, 16>(ctx, recs, tmp, n, st, s);
+  if (R == 40 && K == 16) return run_layout<40, 16>(ctx, recs, tmp, n, st, s);
   set_detail("rec_size=%u key_size=%u not built", R, K);
   return RADSORT_ERR_UNSUPPORTED;
 }
@@ -91,7 +100,7 @@ static radsort_status check_layout(uint32_t R, uint32_t K) {
     set_detail("rec_size must be a multiple of 8 in [key_size, 64] (got %u)", R);
     return RADSORT_ERR_INVALID_ARG;
   }
-  if (!((R == 8 && K == 8) || R == 16 || R == 32)) {
+  if (!((R == 8 && K == 8) || R == 16 || R == 32 || R == 24 || (R == 40 && K == 16))) {
     set_detail("rec_size=%u key_size=%u is not built", R, K);
     return RADSORT_ERR_UNSUPPORTED;
   }

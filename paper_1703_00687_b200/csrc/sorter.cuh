@@ -49,7 +49,7 @@ struct Sorter {
   // need 512 threads.
   static void launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                            uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
-    constexpr int ILMAX = 256 / R;
+    constexpr int ILMAX = (int)((C + 511) / 512);  // records per thread at 512 threads
     if ((size_t)maxlen > (size_t)256 * ILMAX) {
       launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms);
       return;
@@ -59,11 +59,11 @@ struct Sorter {
     if (il <= 1) RS_LOCAL(1);
     else if (il <= 2) RS_LOCAL(2);
     else if (il <= 4) RS_LOCAL(4);
+    else if constexpr (ILMAX <= 8) RS_LOCAL(ILMAX);
     else if (il <= 8) RS_LOCAL(8);
-    else if constexpr (ILMAX >= 16) {
-      if (il <= 16) RS_LOCAL(16);
-      else if constexpr (ILMAX >= 32) RS_LOCAL(32);
-    }
+    else if constexpr (ILMAX <= 16) RS_LOCAL(ILMAX);
+    else if (il <= 16) RS_LOCAL(16);
+    else RS_LOCAL(ILMAX);
 #undef RS_LOCAL
   }
 
@@ -127,7 +127,7 @@ struct Sorter {
   template <int TB, int SB, int MINB>
   static radsort_status run_cfg(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
                                 radsort_stats& stats) {
-    constexpr uint32_t T = (uint32_t)(TB / R);
+    constexpr uint32_t T = tile_recs<R, TB, SB>();
     set_attrs();
     static bool attr = false;
     if (!attr) {
@@ -168,7 +168,7 @@ struct Sorter {
       ch_tot = (uint32_t*)ctx->mlt.p;
       carry_in = (uint32_t*)ctx->mle.p;
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, TB>, HIST_B, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, T>, HIST_B, 0);
     occ_s = std::max(occ_s, 1);
     occ_h = std::max(occ_h, 1);
 
@@ -201,11 +201,11 @@ struct Sorter {
         const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
         tm.begin(RADSORT_K_HIST);
         if (pre) {
-          k_hist_pre<R, K, TB><<<hist_grid, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp,
+          k_hist_pre<R, K, T><<<hist_grid, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp,
                                                              tile_pre, ch_first, ch_last, ch_tot);
           k_carry<<<1, RADIX, 0, st>>>(ch_first, ch_last, ch_tot, hist_grid, carry_in);
         } else {
-          k_hist<R, K, TB><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
+          k_hist<R, K, T><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
         }
         tm.end();
         tm.begin(RADSORT_K_PLAN);
@@ -302,7 +302,7 @@ template <int R, int K>
 radsort_status multi_hist(Context* ctx, const uint8_t* recs, uint32_t n, uint32_t digit, cudaStream_t st,
                           uint64_t* h256, uint64_t* andor4) {
   using S = Sorter<R, K>;
-  constexpr uint32_t T = MULTI_TB / R;
+  constexpr uint32_t T = tile_recs<R, MULTI_TB, MULTI_SB>();
   workspace_acquire(ctx, st);
   typename S::Views v;
   radsort_status rs = S::prepare(ctx, n > 0 ? n : 1, T, v);
@@ -314,9 +314,9 @@ radsort_status multi_hist(Context* ctx, const uint8_t* recs, uint32_t n, uint32_
   RS_CUDA(cudaMemsetAsync(v.ctl, 0, sizeof(Ctl), st));
   k_prep<<<1, 1024, 0, st>>>(v.L[0], 1, T, v.tile_start, v.ctl, 1);
   int occ_h = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, MULTI_TB>, HIST_B, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, T>, HIST_B, 0);
   const unsigned gh = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_h));
-  k_hist<R, K, MULTI_TB><<<gh, HIST_B, 0, st>>>(v.L[0], v.tile_start, 1, v.ctl, v.hist, v.andor, (const uint8_t*)recs,
+  k_hist<R, K, T><<<gh, HIST_B, 0, st>>>(v.L[0], v.tile_start, 1, v.ctl, v.hist, v.andor, (const uint8_t*)recs,
                                                  (const uint8_t*)recs);
   uint32_t h32[RADIX];
   RS_CUDA(cudaMemcpyAsync(h32, v.hist, sizeof h32, cudaMemcpyDeviceToHost, st));
@@ -331,7 +331,7 @@ template <int R, int K>
 radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, uint32_t digit, const uint64_t* h256,
                              cudaStream_t st) {
   using S = Sorter<R, K>;
-  constexpr uint32_t T = MULTI_TB / R;
+  constexpr uint32_t T = tile_recs<R, MULTI_TB, MULTI_SB>();
   if (n == 0) return RADSORT_OK;
   workspace_acquire(ctx, st);
   typename S::Views v;

@@ -65,7 +65,8 @@ def test_bad_layouts_rejected_before_any_device_work():
     L = rs.lib
     assert L.radsort_sort(None, None, 10, 8, 16, None) == ERR_INVALID_ARG   # K > R
     assert L.radsort_sort(None, None, 10, 12, 8, None) == ERR_INVALID_ARG   # R not multiple of 8
-    assert L.radsort_sort(None, None, 10, 24, 8, None) == ERR_UNSUPPORTED   # not built yet
+    assert L.radsort_sort(None, None, 10, 48, 8, None) == ERR_UNSUPPORTED   # not built
+    assert L.radsort_sort(None, None, 10, 40, 8, None) == ERR_UNSUPPORTED   # not built (SPEC layouts only)
     assert L.radsort_sort(None, None, 10, 8, 4, None) == ERR_INVALID_ARG
 
 

@@ -69,7 +69,8 @@ def _init():
 
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("R,K,dist", [(8, 8, "uniform"), (16, 8, "uniform40"), (8, 8, "zipf"), (32, 16, "uniform"),
-                                      (16, 16, "bytes"), (8, 8, "few"), (16, 8, "equal")])
+                                      (16, 16, "bytes"), (8, 8, "few"), (16, 8, "equal"), (24, 8, "uniform"),
+                                      (40, 16, "zipf")])
 def test_loopback_multi(G, R, K, dist):
     rng = np.random.default_rng(G * 100 + R)
     sizes = [int(x) for x in rng.integers(20_000, 120_000, G)]

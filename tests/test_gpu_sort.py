@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 import oracle  # noqa: E402
 from datagen import host as dg  # noqa: E402
 
-LAYOUTS = [(8, 8), (16, 8), (16, 16), (32, 8), (32, 16)]
+LAYOUTS = [(8, 8), (16, 8), (16, 16), (24, 8), (24, 16), (32, 8), (32, 16), (40, 16)]
 GUARD = 4096
 POISON = 0xA5
 
@@ -25,7 +25,7 @@ def C_of(R):
 
 
 def T_of(R):
-    return 32768 // R  # default scatter tile (RADSORT_SCATTER_CFG=1)
+    return (32768 // R) // 256 * 256  # default scatter tile (RADSORT_SCATTER_CFG=1): a multiple of 256 records
 
 
 def run_gpu_sort(a: np.ndarray, K: int, guard=True):
@@ -81,11 +81,11 @@ def test_capacity_and_tile_boundaries(R, K):
 def test_other_tile_configs(cfg, monkeypatch):
     # every scatter/histogram tile configuration and the look-back variant stay exact
     monkeypatch.setenv("RADSORT_SCATTER_CFG", cfg)
-    for R, K in ((8, 8), (16, 8), (32, 16)):
+    for R, K in ((8, 8), (16, 8), (24, 8), (32, 16), (40, 16)):
         check(dg.generate(400_003, R, K, "uniform", seed=11), K)
         check(dg.generate(200_001, R, K, "few", payload="index" if R > K else "random", seed=12), K)
     monkeypatch.setenv("RADSORT_LOOKBACK", "1")
-    for R, K in ((8, 8), (16, 8), (32, 16)):
+    for R, K in ((8, 8), (16, 8), (24, 16), (32, 16)):
         check(dg.generate(400_003, R, K, "zipf", seed=13), K)
 
 
