@@ -75,6 +75,8 @@ typedef struct {
   uint32_t kernel_launches[RADSORT_K_COUNT];
   float kernel_ms[RADSORT_K_COUNT];
   uint64_t kernel_bytes[RADSORT_K_COUNT]; /* algorithmic HBM bytes (read + write)      */
+  uint64_t bins_split;        /* segments split three ways around a dominant key        */
+  uint64_t records_split;     /* records of those dominant keys (final after the split) */
 } radsort_stats;
 
 /* Create the per-(process, device) context for `device` (cudaSetDevice is the

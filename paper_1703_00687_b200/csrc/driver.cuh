@@ -39,6 +39,7 @@ struct Context {
   std::mutex mu;
   // workspace
   DevBuf large[2], local[2], hist, andor, segbase, tile_start, status, ctl, host_io[2];
+  DevBuf splitc, probes;  // dominant-key split: per-segment class cursors; keys of the bins to fill
   Ctl* h_ctl = nullptr;  // pinned
   uint32_t epoch = 0;
   cudaEvent_t ev[2 * 64] = {};

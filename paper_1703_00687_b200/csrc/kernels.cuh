@@ -10,6 +10,7 @@
 // Shares no code with oracle/ or datagen/.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace radsort {
@@ -25,11 +26,12 @@ template <int R> __host__ __device__ constexpr uint32_t local_capacity() { retur
 template <int R, int TB, int SB> __host__ __device__ constexpr uint32_t tile_recs() { return (uint32_t)((TB / R) / SB * SB); }
 
 enum : uint8_t { SRC_REC = 0, SRC_TMP = 1 };
-enum : uint8_t { MODE_NONE = 0, MODE_SCATTER = 1, MODE_COPY = 2 };
-enum : uint8_t { FLAG_EQUAL = 1 };
+enum : uint8_t { MODE_NONE = 0, MODE_SCATTER = 1, MODE_COPY = 2, MODE_SPLIT = 3, MODE_FILL = 4 };
+enum : uint8_t { FLAG_EQUAL = 1, FLAG_FILL = 2, FLAG_CAND = 4 };  // CAND: sampled as possibly key-dominated
 
 // A bin ("bins that may be further processed independently"):
 // record range [off, off+len) of buffer `src`, to be partitioned by digit `depth`.
+// `aux`: for a FLAG_FILL bin, the index of its key in the probe-key table.
 struct Seg {
   uint32_t off;
   uint32_t len;
@@ -37,7 +39,7 @@ struct Seg {
   uint8_t src;
   uint8_t mode;
   uint8_t flags;
-  uint32_t pad;
+  uint32_t aux;
 };
 static_assert(sizeof(Seg) == 16, "Seg is 16 bytes");
 
@@ -51,6 +53,8 @@ struct Ctl {
   uint32_t d0;             // first digit of the level-0 pass (from k_sample)
   unsigned long long rec_hist, rec_scatter, rec_copy, rec_tiny, rec_local, rec_final;
   unsigned long long bins_large, bins_local, bins_tiny, bins_final;
+  unsigned long long bins_split, rec_split;  // dominant-key three-way splits (segments, records of the key)
+  uint32_t n_probe;                          // probe-key table entries used this sort
   unsigned long long prof[16];  // phase cycle counters (RADSORT_PHASE_PROF builds only)
 };
 
@@ -125,6 +129,15 @@ template <> __device__ __forceinline__ Key<16> key_of<32, 16>(const Rec<32>& r) 
 template <> __device__ __forceinline__ Key<8> key_of<24, 8>(const Rec<24>& r) { return {u64of(r.a.x, r.a.y)}; }
 template <> __device__ __forceinline__ Key<16> key_of<24, 16>(const Rec<24>& r) { return {u64of(r.a.x, r.a.y), u64of(r.b.x, r.b.y)}; }
 template <> __device__ __forceinline__ Key<16> key_of<40, 16>(const Rec<40>& r) { return {u64of(r.a.x, r.a.y), u64of(r.b.x, r.b.y)}; }
+
+// The record whose bytes are exactly a key (R == K; used to fill final bins).
+template <int R, int K> __device__ __forceinline__ Rec<R> rec_of_key(const Key<K>& k) {
+  Rec<R> x{};
+  if constexpr (R == 8 && K == 8) x.a = make_uint2((uint32_t)k.w0, (uint32_t)(k.w0 >> 32));
+  if constexpr (R == 16 && K == 16)
+    x.a = make_uint4((uint32_t)k.w0, (uint32_t)(k.w0 >> 32), (uint32_t)k.w1, (uint32_t)(k.w1 >> 32));
+  return x;
+}
 
 // Digit d, d = 0 most significant ("1 B digits"): byte K-1-d.
 __device__ __forceinline__ uint32_t digit_of(const Key<8>& k, uint32_t d) {

@@ -111,6 +111,25 @@ static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint3
   }
 }
 
+// -------------------------------------------------------------- k_cand
+// One warp per Large segment: 32 keys sampled evenly across the segment are
+// compared with its first key; 12 or more matches flag the segment as
+// possibly dominated by that key (FLAG_CAND), and only flagged segments pay
+// for counting the exact equal/below counts in k_hist_pre (k_plan decides).
+template <int R, int K>
+__global__ void k_cand(Seg* segs, uint32_t nseg, const uint8_t* recs, const uint8_t* tmp) {
+  const uint32_t s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= nseg) return;
+  const Seg sg = segs[s];
+  if (sg.flags & (FLAG_EQUAL | FLAG_FILL)) return;
+  const uint8_t* b = (sg.src == SRC_TMP ? tmp : recs) + (size_t)sg.off * R;
+  const Key<K> k0 = ld_key<R, K>(b);
+  const Key<K> kj = ld_key<R, K>(b + (size_t)((uint64_t)sg.len * (uint32_t)lane / 32u) * R);
+  const int votes = __popc(__ballot_sync(0xffffffffu, key_eq(kj, k0)));
+  if (lane == 0) segs[s].flags = (uint8_t)((sg.flags & ~FLAG_CAND) | (votes >= 12 ? FLAG_CAND : 0));
+}
+
 // -------------------------------------------------------------- k_hist
 // Per-segment histogram of the segment's digit + AND/OR of its keys, one read
 // of the data ("counting sort may be applied per single phase").
@@ -157,8 +176,8 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
       h[i] = 0;
     }
     if (tid < KW) {
-      if (sna[tid]) atomicOr(&andor[(size_t)s * 4 + tid], sna[tid]);
-      if (so[tid]) atomicOr(&andor[(size_t)s * 4 + 2 + tid], so[tid]);
+      if (sna[tid]) atomicOr(&andor[(size_t)s * 8 + tid], sna[tid]);
+      if (so[tid]) atomicOr(&andor[(size_t)s * 8 + 2 + tid], so[tid]);
     }
     __syncthreads();
     if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
@@ -170,7 +189,7 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
       cur_end = tile_start[cur + 1];
     }
     const Seg sg = segs[cur];
-    if (sg.flags & FLAG_EQUAL) continue;
+    if (sg.flags & (FLAG_EQUAL | FLAG_FILL)) continue;
     const uint32_t lt = t - tile_start[cur];
     const uint32_t m = min(T, sg.len - lt * T);
     const uint8_t* src = (sg.src == SRC_TMP ? tmp : recs) + (size_t)(sg.off + lt * T) * R;
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
 // (k_carry turns these into each chunk's carry-in).
 constexpr uint32_t NO_SEG = 0xffffffffu;
 template <int R, int K, uint32_t T>
-__global__ void __launch_bounds__(HIST_B) k_hist_pre(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
+__global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                      uint32_t nseg, const Ctl* __restrict__ ctl,
                                                      uint32_t* __restrict__ hist, unsigned long long* __restrict__ andor,
                                                      const uint8_t* recs, const uint8_t* tmp, uint32_t* __restrict__ tile_pre,
@@ -231,11 +250,21 @@ __global__ void __launch_bounds__(HIST_B) k_hist_pre(const Seg* __restrict__ seg
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
   __syncthreads();
   uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+  uint32_t n_eq = 0, n_lt = 0;  // keys equal to / below the segment's probe key
   unsigned long long cnt_recs = 0;
   uint32_t cur = seg_of_tile(tile_start, nseg, t0);
   uint32_t cur_end = tile_start[cur + 1];
+  Key<K> probe{};
+  uint32_t probe_seg = NO_SEG;  // the probe (first record's key) is loaded once per segment
   if (tid == 0) ch_first[c] = cur;
   auto flush = [&](uint32_t s) {
+    {
+      const uint32_t e = __reduce_add_sync(0xffffffffu, n_eq), l = __reduce_add_sync(0xffffffffu, n_lt);
+      if (lane == 0 && e) atomicAdd(&andor[(size_t)s * 8 + 4], (unsigned long long)e);
+      if (lane == 0 && l) atomicAdd(&andor[(size_t)s * 8 + 5], (unsigned long long)l);
+      n_eq = 0;
+      n_lt = 0;
+    }
 #pragma unroll
     for (int w = 0; w < KW; ++w) {
       const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
@@ -252,8 +281,8 @@ __global__ void __launch_bounds__(HIST_B) k_hist_pre(const Seg* __restrict__ seg
       run[i] = 0;
     }
     if (tid < KW) {
-      if (sna[tid]) atomicOr(&andor[(size_t)s * 4 + tid], sna[tid]);
-      if (so[tid]) atomicOr(&andor[(size_t)s * 4 + 2 + tid], so[tid]);
+      if (sna[tid]) atomicOr(&andor[(size_t)s * 8 + tid], sna[tid]);
+      if (so[tid]) atomicOr(&andor[(size_t)s * 8 + 2 + tid], so[tid]);
     }
     __syncthreads();
     if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
@@ -265,25 +294,53 @@ __global__ void __launch_bounds__(HIST_B) k_hist_pre(const Seg* __restrict__ seg
       cur_end = tile_start[cur + 1];
     }
     const Seg sg = segs[cur];
-    if (sg.flags & FLAG_EQUAL) continue;
+    if (sg.flags & (FLAG_EQUAL | FLAG_FILL)) continue;
     const uint32_t lt = t - tile_start[cur];
     const uint32_t m = min(T, sg.len - lt * T);
-    const uint8_t* src = (sg.src == SRC_TMP ? tmp : recs) + (size_t)(sg.off + lt * T) * R;
+    const uint8_t* sbase = (sg.src == SRC_TMP ? tmp : recs) + (size_t)sg.off * R;
+    const uint8_t* src = sbase + (size_t)lt * T * R;
+    if ((sg.flags & FLAG_CAND) && probe_seg != cur) {
+      probe = ld_key<R, K>(sbase);
+      probe_seg = cur;
+    }
     const uint32_t d = sg.depth;
-    for (uint32_t i0 = tid; i0 < m; i0 += HIST_B * U) {
-      Key<K> k[U];
+    if (!(sg.flags & FLAG_CAND)) {
+      for (uint32_t i0 = tid; i0 < m; i0 += HIST_B * U) {
+        Key<K> k[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t i = i0 + u * HIST_B;
-        if (i < m) k[u] = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = i0 + u * HIST_B;
+          if (i < m) k[u] = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = i0 + u * HIST_B;
+          if (i < m) {
+            atomicAdd(&h[digit_of(k[u], d)], 1u);
+            na[0] |= ~k[u].w0; o[0] |= k[u].w0;
+            if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
+          }
+        }
       }
+    } else {  // a candidate for the dominant-key split: also count keys equal to / below the probe
+      constexpr int U2 = U / 4;
+      for (uint32_t i0 = tid; i0 < m; i0 += HIST_B * U2) {
+        Key<K> k[U2];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t i = i0 + u * HIST_B;
-        if (i < m) {
-          atomicAdd(&h[digit_of(k[u], d)], 1u);
-          na[0] |= ~k[u].w0; o[0] |= k[u].w0;
-          if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
+        for (int u = 0; u < U2; ++u) {
+          const uint32_t i = i0 + u * HIST_B;
+          if (i < m) k[u] = key_of<R, K>(ldg_rec<R>(src + (size_t)i * R));
+        }
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+          const uint32_t i = i0 + u * HIST_B;
+          if (i < m) {
+            atomicAdd(&h[digit_of(k[u], d)], 1u);
+            na[0] |= ~k[u].w0; o[0] |= k[u].w0;
+            if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
+            n_eq += (uint32_t)key_eq(k[u], probe);
+            n_lt += (uint32_t)key_lt(k[u], probe);
+          }
         }
       }
     }
@@ -334,20 +391,27 @@ static __global__ void __launch_bounds__(RADIX) k_carry(const uint32_t* __restri
 
 // -------------------------------------------------------------- k_plan
 // Per Large segment: constant-digit skip / all-equal detection,
-// bin bases = exclusive prefix of the histogram.
-template <int K>
-__global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __restrict__ hist,
+// bin bases = exclusive prefix of the histogram.  A segment in
+// which more than half of the records carry its first record's key (a
+// dominant key: skewed inputs, PAPER.md:247 Zipf) is split three ways instead
+// -- keys below / equal to / above that key -- so the dominant key's records
+// are final after one pass rather than being carried through every later
+// level with the few other keys of their bin ("bins with all keys
+// equal" generalised to "all but a few").  andor[s] holds 8
+// words: ~AND (2), OR (2), #keys == probe, #keys < probe (k_hist_pre).
+template <int R, int K>
+__global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict__ hist,
                                                 const unsigned long long* __restrict__ andor,
                                                 uint32_t* __restrict__ segbase, Seg* large_next, Ctl* ctl,
-                                                int force = 0) {
+                                                uint32_t* __restrict__ splitc, int split_ok, int force = 0) {
   __shared__ uint32_t ws[8];
   __shared__ int sh_const;
   const uint32_t s = blockIdx.x;
   const int tid = threadIdx.x;
   const Seg sg = segs[s];
-  if (sg.flags & FLAG_EQUAL) {  // known all-equal final bin: copy tmp -> records if needed
+  if (sg.flags & (FLAG_EQUAL | FLAG_FILL)) {  // known final bin: copied tmp -> records / filled with its key
     if (tid == 0) {
-      segs[s].mode = sg.src == SRC_TMP ? MODE_COPY : MODE_NONE;
+      segs[s].mode = (sg.flags & FLAG_FILL) ? MODE_FILL : (sg.src == SRC_TMP ? MODE_COPY : MODE_NONE);
       atomicAdd(&ctl->rec_final, (unsigned long long)sg.len);
     }
     return;
@@ -357,10 +421,11 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __res
   const uint32_t c = hist[(size_t)s * RADIX + tid];
   if (c == sg.len && !force) sh_const = 1;
   __syncthreads();
+  const unsigned long long* ao = andor + (size_t)s * 8;
   if (sh_const) {
     if (tid == 0) {
       uint64_t A[2], O[2];
-      for (int w = 0; w < K / 8; ++w) { A[w] = ~andor[(size_t)s * 4 + w]; O[w] = andor[(size_t)s * 4 + 2 + w]; }
+      for (int w = 0; w < K / 8; ++w) { A[w] = ~ao[w]; O[w] = ao[2 + w]; }
       const uint32_t d2 = first_nonconst_digit<K>(A, O, sg.depth);
       if (d2 >= (uint32_t)K) {  // all keys equal: final
         segs[s].mode = sg.src == SRC_TMP ? MODE_COPY : MODE_NONE;
@@ -375,9 +440,69 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, const uint32_t* __res
     }
     return;
   }
+  const uint32_t n_eq = (uint32_t)ao[4], n_lt = (uint32_t)ao[5];
+  // the equal records become final: written straight to `records` when the
+  // segment sits in tmp; when it sits in `records` they can only be skipped
+  // and re-filled (records that are all key, R == K)
+  if (split_ok && (sg.flags & FLAG_CAND) && 2ull * n_eq > sg.len && (sg.src == SRC_TMP || R == K)) {
+    __syncthreads();
+    hist[(size_t)s * RADIX + tid] = tid == 0 ? n_lt : tid == 1 ? n_eq : tid == 2 ? sg.len - n_lt - n_eq : 0u;
+    if (tid < 3) segbase[(size_t)s * RADIX + tid] = sg.off + (tid >= 1 ? n_lt : 0u) + (tid == 2 ? n_eq : 0u);
+    if (tid < 4) splitc[(size_t)s * 4 + tid] = 0;
+    if (tid == 0) {
+      segs[s].mode = MODE_SPLIT;
+      atomicAdd(&ctl->bins_split, 1ull);
+      atomicAdd(&ctl->rec_split, (unsigned long long)n_eq);
+    }
+    return;
+  }
   const uint32_t ex = block_excl_scan256(c, ws);
   segbase[(size_t)s * RADIX + tid] = sg.off + ex;
   if (tid == 0) segs[s].mode = MODE_SCATTER;
+}
+
+// One tile of a MODE_SPLIT segment (k_plan): three-way split around the
+// segment's dominant key -- class 0/1/2 = key below / equal to / above it.
+// Ranks by warp match + one smem atomic per class and warp; each class's range
+// is reserved per tile with one global atomic (order inside a class is free,
+// DESIGN.md R2).  The equal class is final: written to `records` (segment in
+// tmp), or skipped and filled later (segment in `records`, R == K).  Reads the
+// tile twice (L2 hits; rare tiles) and is kept out of line so the digit
+// scatter's register allocation does not pay for it.  Every thread calls it.
+template <int R, int K, int SB>
+__device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base, uint32_t m, uint8_t* dst,
+                                        uint8_t* recs, uint8_t* tmp, const uint32_t* __restrict__ segbase,
+                                        uint32_t* __restrict__ splitc, uint8_t* stage, uint32_t* cnt,
+                                        uint32_t* gofs) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint8_t* sb = buf_of(sg.src, recs, tmp);
+  const uint8_t* src = sb + (size_t)base * R;
+  const Key<K> probe = ld_key<R, K>(sb + (size_t)sg.off * R);
+  uint32_t* rkv = reinterpret_cast<uint32_t*>(stage);  // per-record class << 16 | rank (T * 4 <= TB bytes)
+  const uint32_t lanelt = (1u << lane) - 1u;
+  for (uint32_t q0 = 0; q0 < m; q0 += SB) {
+    const uint32_t q = q0 + tid;
+    uint32_t cl = 3u;
+    if (q < m) {
+      const Key<K> kx = ld_key<R, K>(src + (size_t)q * R);
+      cl = key_lt(kx, probe) ? 0u : (key_eq(kx, probe) ? 1u : 2u);
+    }
+    const uint32_t mk = __match_any_sync(0xffffffffu, cl);
+    const int leader = __ffs(mk) - 1;
+    uint32_t b = 0;
+    if (lane == leader && cl < 3u) b = atomicAdd(&cnt[cl], (uint32_t)__popc(mk));
+    b = __shfl_sync(0xffffffffu, b, leader);
+    if (q < m) rkv[q] = (b + (uint32_t)__popc(mk & lanelt)) | (cl << 16);
+  }
+  __syncthreads();
+  if (tid < 3) gofs[tid] = segbase[(size_t)s * RADIX + tid] + atomicAdd(&splitc[(size_t)s * 4 + tid], cnt[tid]);
+  __syncthreads();
+  const bool eq_skip = sg.src == SRC_REC;  // R == K: the equal run is filled later
+  for (uint32_t q = tid; q < m; q += SB) {
+    const uint32_t v = rkv[q], cl = v >> 16;
+    if (cl == 1u && eq_skip) continue;
+    st_rec<R>((cl == 1u ? recs : dst) + (size_t)(gofs[cl] + (v & 0xffffu)) * R, ldg_rec<R>(src + (size_t)q * R));
+  }
 }
 
 // -------------------------------------------------------------- k_scatter
@@ -393,7 +518,9 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
                                                        uint8_t* recs, uint8_t* tmp, const uint32_t* __restrict__ tile_pre,
                                                        const uint32_t* __restrict__ ch_first,
-                                                       const uint32_t* __restrict__ carry_in, uint32_t hist_grid) {
+                                                       const uint32_t* __restrict__ carry_in, uint32_t hist_grid,
+                                                       uint32_t* __restrict__ splitc,
+                                                       const unsigned long long* __restrict__ probes) {
   constexpr uint32_t T = tile_recs<R, TB, SB>();
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
@@ -527,12 +654,38 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       moved += m;
       t = tn;
       s = sn;
+    } else if (sg.mode == MODE_SPLIT) {
+      // three-way split around the segment's dominant key (k_plan): class
+      // 0/1/2 = key below / equal to / above it.  Ranks by warp ballots; each
+      // class's range is reserved per tile with one atomic (order inside a
+      // class is free, R2); each warp stores its records of a class
+      // as one contiguous run, straight from registers.  The equal class is
+      // final: written to `records` (segment in tmp), or skipped and filled
+      // later (segment in `records`, R == K).
+      if (tid == 0) take();  // next ticket (ordered before the barriers inside)
+      split_tile<R, K, SB>(sg, s, base, m, dst, recs, tmp, segbase, splitc, stage, cnt, gofs);
+      __syncthreads();  // sh_t/sh_s hold the next ticket; cnt / gofs / stage reusable
+      const uint32_t tn = sh_t, sn = sh_s;
+      if (tid < RADIX) cnt[tid] = 0;
+      if (tn < total) load(tn, sn);
+      moved += m;
+      t = tn;
+      s = sn;
     } else {
       if (sg.mode == MODE_COPY) {
         const uint8_t* src = buf_of(sg.src, recs, tmp);
         for (uint32_t i = tid; i < m; i += SB)
           st_rec<R>(dst + (size_t)(base + i) * R, ldg_rec<R>(src + (size_t)(base + i) * R));
         moved += m;
+      } else if (sg.mode == MODE_FILL) {  // write-only: every record of the bin is its (dominant) key
+        if constexpr (R == K) {
+          Key<K> kf;
+          kf.w0 = probes[(size_t)sg.aux * 2];
+          if constexpr (K == 16) kf.w1 = probes[(size_t)sg.aux * 2 + 1];
+          const Rec<R> x = rec_of_key<R, K>(kf);
+          for (uint32_t i = tid; i < m; i += SB) st_rec<R>(recs + (size_t)(base + i) * R, x);
+          moved += m / 2;  // write-only: R bytes per record
+        }
       }
       if (tid == 0) take();
       __syncthreads();
@@ -562,7 +715,8 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
 template <int R, int K>
 __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
-                                                      Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
+                                                      Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
+                                                      unsigned long long* __restrict__ probes) {
   enum : uint8_t { C_NONE = 0, C_COPY = 1, C_ES = 2, C_TINY = 3 };
   extern __shared__ uint4 smem_raw[];
   __shared__ uint8_t cls[RADIX];
@@ -570,11 +724,12 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
   __shared__ __align__(16) TailScratch<K> wsc[CHILD_B / 32];
   const uint32_t s = blockIdx.x;
   const Seg sg = segs[s];
-  if (sg.mode != MODE_SCATTER) return;
+  if (sg.mode != MODE_SCATTER && sg.mode != MODE_SPLIT) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* scratch = reinterpret_cast<uint8_t*>(smem_raw) + (size_t)warp * TINY_MAX * R;
   const uint8_t loc = sg.src == SRC_TMP ? SRC_REC : SRC_TMP;  // children live where the scatter wrote
-  const uint32_t d1 = sg.depth + 1u;
+  const bool split = sg.mode == MODE_SPLIT;  // children 0/1/2: below / equal to / above the dominant key
+  const uint32_t d1 = split ? sg.depth : sg.depth + 1u;
   constexpr uint32_t C = local_capacity<R>();
   uint8_t* cbuf = buf_of(loc, recs, tmp);
   if (tid < RADIX) {
@@ -582,6 +737,17 @@ __global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ se
     const uint32_t off = segbase[(size_t)s * RADIX + tid];
     uint8_t c = C_NONE;
     if (len == 0) {
+    } else if (split && tid == 1) {  // the dominant key: final (written to records, or filled below)
+      if (sg.src == SRC_REC) {
+        const uint32_t pi = atomicAdd(&ctl->n_probe, 1u);
+        const Key<K> pk = ld_key<R, K>(recs + (size_t)sg.off * R);  // untouched by the split scatter
+        probes[(size_t)pi * 2] = pk.w0;
+        if constexpr (K == 16) probes[(size_t)pi * 2 + 1] = pk.w1;
+        Seg ns = {off, len, (uint8_t)K, SRC_REC, MODE_NONE, FLAG_FILL, pi};
+        large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+      }
+      atomicAdd(&ctl->rec_final, (unsigned long long)len);
+      atomicAdd(&ctl->bins_final, 1ull);
     } else if (d1 >= (uint32_t)K || len == 1) {  // all digits consumed / singleton: final
       if (loc == SRC_TMP) {
         if (len <= C) c = C_COPY;

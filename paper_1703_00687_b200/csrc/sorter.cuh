@@ -71,7 +71,8 @@ struct Sorter {
     Seg* L[2];
     Seg* Lo[2];
     uint32_t *hist, *segbase, *tile_start;
-    unsigned long long *andor, *status;
+    unsigned long long *andor, *status, *probes;
+    uint32_t* splitc;
     Ctl* ctl;
     size_t tiles_max;
   };
@@ -88,7 +89,9 @@ struct Sorter {
     if ((rs = ensure(ctx->local[1], capLoc * sizeof(Seg)))) return rs;
     if ((rs = ensure(ctx->hist, capL * RADIX * sizeof(uint32_t)))) return rs;
     if ((rs = ensure(ctx->segbase, capL * RADIX * sizeof(uint32_t)))) return rs;
-    if ((rs = ensure(ctx->andor, capL * 4 * sizeof(unsigned long long)))) return rs;
+    if ((rs = ensure(ctx->andor, capL * 8 * sizeof(unsigned long long)))) return rs;
+    if ((rs = ensure(ctx->splitc, capL * 4 * sizeof(uint32_t)))) return rs;
+    if ((rs = ensure(ctx->probes, capL * 2 * sizeof(unsigned long long)))) return rs;
     if ((rs = ensure(ctx->tile_start, (capL + 1) * sizeof(uint32_t)))) return rs;
     const size_t old_status = ctx->status.bytes;
     if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
@@ -102,6 +105,8 @@ struct Sorter {
     v.hist = (uint32_t*)ctx->hist.p;
     v.segbase = (uint32_t*)ctx->segbase.p;
     v.andor = (unsigned long long*)ctx->andor.p;
+    v.splitc = (uint32_t*)ctx->splitc.p;
+    v.probes = (unsigned long long*)ctx->probes.p;
     v.tile_start = (uint32_t*)ctx->tile_start.p;
     v.status = (unsigned long long*)ctx->status.p;
     v.ctl = (Ctl*)ctx->ctl.p;
@@ -193,7 +198,7 @@ struct Sorter {
       const int nxt = cur ^ 1;
       if (n_large) {
         RS_CUDA(cudaMemsetAsync(hist, 0, (size_t)n_large * RADIX * sizeof(uint32_t), st));
-        RS_CUDA(cudaMemsetAsync(andor, 0, (size_t)n_large * 4 * sizeof(unsigned long long), st));
+        RS_CUDA(cudaMemsetAsync(andor, 0, (size_t)n_large * 8 * sizeof(unsigned long long), st));
         tm.begin(RADSORT_K_PLAN);
         k_prep<<<1, 1024, 0, st>>>(L[cur], n_large, T, tile_start, ctl, nxt);
         tm.end();
@@ -201,6 +206,7 @@ struct Sorter {
         const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
         tm.begin(RADSORT_K_HIST);
         if (pre) {
+          k_cand<R, K><<<(n_large + 7) / 8, 256, 0, st>>>(L[cur], n_large, recs, tmp);
           k_hist_pre<R, K, T><<<hist_grid, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp,
                                                              tile_pre, ch_first, ch_last, ch_tot);
           k_carry<<<1, RADIX, 0, st>>>(ch_first, ch_last, ch_tot, hist_grid, carry_in);
@@ -209,7 +215,7 @@ struct Sorter {
         }
         tm.end();
         tm.begin(RADSORT_K_PLAN);
-        k_plan<K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl);
+        k_plan<R, K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl, v.splitc, pre ? 1 : 0);
         tm.end();
         if (++ctx->epoch >= 65536) {
           RS_CUDA(cudaMemsetAsync(status, 0, ctx->status.bytes, st));
@@ -220,14 +226,15 @@ struct Sorter {
         if (pre)
           k_scatter<R, K, TB, SB, MINB, true><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
                                                                   ctx->epoch, ctl, recs, tmp, tile_pre, ch_first,
-                                                                  carry_in, hist_grid);
+                                                                  carry_in, hist_grid, v.splitc, v.probes);
         else
           k_scatter<R, K, TB, SB, MINB, false><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
                                                                    ctx->epoch, ctl, recs, tmp, nullptr, nullptr,
-                                                                   nullptr, 0);
+                                                                   nullptr, 0, v.splitc, v.probes);
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
-        k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs, tmp);
+        k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
+                                                                  tmp, v.probes);
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
         stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry
@@ -278,6 +285,8 @@ struct Sorter {
     stats.bins_local = c.bins_local;
     stats.bins_tiny = c.bins_tiny;
     stats.bins_final = c.bins_final;
+    stats.bins_split = c.bins_split;
+    stats.records_split = c.rec_split;
     stats.kernel_bytes[RADSORT_K_HIST] = c.rec_hist * R;
     stats.kernel_bytes[RADSORT_K_SCATTER] = 2ull * c.rec_scatter * R;
     stats.kernel_bytes[RADSORT_K_LOCAL] = 2ull * c.rec_local * R;
@@ -350,7 +359,7 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   RS_CUDA(cudaMemcpyAsync(v.hist, h32, sizeof h32, cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemsetAsync(v.ctl, 0, sizeof(Ctl), st));
   k_prep<<<1, 1024, 0, st>>>(v.L[0], 1, T, v.tile_start, v.ctl, 1);
-  k_plan<K><<<1, RADIX, 0, st>>>(v.L[0], v.hist, v.andor, v.segbase, v.L[1], v.ctl, 1);
+  k_plan<R, K><<<1, RADIX, 0, st>>>(v.L[0], v.hist, v.andor, v.segbase, v.L[1], v.ctl, v.splitc, 0, 1);
   if (++ctx->epoch >= 65536) {
     RS_CUDA(cudaMemsetAsync(v.status, 0, ctx->status.bytes, st));
     ctx->epoch = 1;
@@ -360,7 +369,8 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
                                                 MULTI_SB, MULTI_TB);
   const unsigned gs = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_s));
   k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false><<<gs, MULTI_SB, MULTI_TB, st>>>(
-      v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, nullptr, nullptr, nullptr, 0);
+      v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, nullptr, nullptr, nullptr, 0,
+      v.splitc, v.probes);
   RS_CUDA(cudaGetLastError());
   RS_CUDA(cudaStreamSynchronize(st));
   workspace_release(ctx, st);

@@ -36,6 +36,7 @@ class Stats(ctypes.Structure):
         ("nvlink_bytes_sent", ctypes.c_uint64), ("nvlink_bytes_recv", ctypes.c_uint64),
         ("kernel_launches", ctypes.c_uint32 * 7), ("kernel_ms", ctypes.c_float * 7),
         ("kernel_bytes", ctypes.c_uint64 * 7),
+        ("bins_split", ctypes.c_uint64), ("records_split", ctypes.c_uint64),
     ]
 
 

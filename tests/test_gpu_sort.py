@@ -159,3 +159,43 @@ def test_stats_report_constant_digit_skip():
     w = got.view(np.uint64).reshape(-1, 2)
     assert np.all(w[1:, 0] >= w[:-1, 0])
     assert np.array_equal(np.sort(w[:, 1]), np.arange(1_000_000, dtype=np.uint64))
+
+
+def _dominate(a: np.ndarray, K: int, frac_num: int, frac_den: int, key_words, offset: int = 0):
+    """Overwrite the key of frac_num out of every frac_den records (from `offset`) with key_words."""
+    w = a.view(np.uint64).reshape(a.shape[0], -1)
+    for j in range(frac_num):
+        for k, kw in enumerate(key_words):
+            w[offset + j::frac_den, k] = np.uint64(kw)
+    return a
+
+
+@pytest.mark.parametrize("R,K", LAYOUTS)
+@pytest.mark.parametrize("n", [40_000, 300_001, 2_000_003])
+def test_dominant_key_split(R, K, n):
+    # a key holding 60 % of the records dominates the level-0 segment and its
+    # level-1 bin; a second key with 25 % shares its top byte (nested split);
+    # the rest uniform.  Exercises the three-way split with the equal run
+    # written to `records` (segment in tmp) and skipped + filled (R == K,
+    # segment in `records`), and the below/above remainders at the same depth.
+    import paper_1703_00687_b200 as rs
+
+    a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=n + R)
+    top = [0x5A00_1234_5678_9ABC] if K == 8 else [0x0123_4567_89AB_CDEF, 0x5A00_1234_5678_9ABC]
+    sec = [0x5A77_0000_0000_0001] if K == 8 else [0x0, 0x5A77_0000_0000_0001]
+    _dominate(a, K, 3, 5, top)
+    _dominate(a, K, 1, 8, sec, offset=3)
+    check(a, K)
+    st = rs.last_stats()
+    if n >= 300_001:
+        assert st["bins_split"] >= 1 and st["records_split"] > 0
+
+
+def test_dominant_key_split_zipf_stats():
+    # Zipf keys (c3 recipe): heavy keys are split off, and the result is exact
+    import paper_1703_00687_b200 as rs
+
+    a = dg.generate(3_000_000, 8, 8, "zipf", seed=99)
+    check(a, 8)
+    st = rs.last_stats()
+    assert st["bins_split"] >= 1
