@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
 // (§3.3); <= C -> Local list; larger -> next level's Large
 // list.  Dynamic smem: one TINY_MAX*R scratch per warp.
 template <int R, int K>
-__global__ void __launch_bounds__(CHILD_B) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
+__global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
                                                       Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
                                                       unsigned long long* __restrict__ probes) {
