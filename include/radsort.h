@@ -175,6 +175,19 @@ void radsort_finalize(void);
 /* Library version, e.g. "radsort 0.1 sm_100a". */
 const char* radsort_version(void);
 
+/* Tiny-sorter benchmark (the GPU analog of PAPER.md:193-232 §4.1, Fig. 1;
+ * benchmark infrastructure, not on the sort path): `bins` arrays of n
+ * records (rec_size, key_size in {(8,8), (16,8), (16,16), (32,8), (32,16)}),
+ * keys sharing their top digit, are sorted in device memory by algorithm
+ * `algo` -- 0 enumeration sort (n <= 32), 1 warp bitonic network, 2 warp
+ * tail sorter (counting pass + ES among colliders), 3 insertion sort, one
+ * thread per array -- for 2 <= n <= 128.  *ns_per_record = best of 3 timed
+ * runs (CUDA events) / (bins * n).  The output is checked on the device
+ * (RADSORT_ERR_CUDA with detail if any array is out of order).  Allocates
+ * and frees its own device memory on the current device. */
+radsort_status radsort_tinybench(uint32_t rec_size, uint32_t key_size, uint32_t n, uint32_t algo,
+                                 uint64_t bins, double* ns_per_record);
+
 #ifdef __cplusplus
 }
 #endif

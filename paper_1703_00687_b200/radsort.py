@@ -20,7 +20,7 @@ KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "mul
 EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
            "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
            "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
-           "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split"]
+           "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench"]
 
 
 class Stats(ctypes.Structure):
@@ -70,9 +70,11 @@ def _load():
     L.radsort_plan_quotas.argtypes = [u64, i32, vp]
     L.radsort_plan_digit.argtypes = [vp, u64, ctypes.POINTER(u32)]
     L.radsort_plan_equal_split.argtypes = [vp, i32, u64, u64, vp]
+    L.radsort_tinybench.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(ctypes.c_double)]
     for f in ("radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
               "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
-              "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split"):
+              "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split",
+              "radsort_tinybench"):
         getattr(L, f).restype = i32
     return L
 
@@ -227,3 +229,14 @@ def last_stats() -> dict:
 
 def finalize() -> None:
     lib.radsort_finalize()
+
+
+TINY_ALGOS = {0: "enumeration sort (lane per record)", 1: "warp bitonic network", 2: "warp tail sorter",
+              3: "insertion sort (thread per array)"}
+
+
+def tinybench(rec_size: int, key_size: int, n: int, algo: int, bins: int = 1 << 18) -> float:
+    """ns per record of tiny-sorter `algo` on `bins` arrays of n records (radsort_tinybench)."""
+    out = ctypes.c_double(0.0)
+    _check(lib.radsort_tinybench(rec_size, key_size, n, algo, bins, ctypes.byref(out)))
+    return out.value

@@ -199,3 +199,15 @@ def test_dominant_key_split_zipf_stats():
     check(a, 8)
     st = rs.last_stats()
     assert st["bins_split"] >= 1
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (32, 16)])
+def test_tinybench_sorters_are_correct(R, K):
+    # every tiny sorter sorts every array (the device check inside raises otherwise)
+    import paper_1703_00687_b200 as rs
+
+    for n in (2, 3, 17, 32, 33, 64, 65, 100, 128):
+        for algo in (0, 1, 2, 3):
+            if algo == 0 and n > 32:
+                continue
+            assert rs.tinybench(R, K, n, algo, bins=4096) > 0.0
