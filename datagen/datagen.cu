@@ -67,6 +67,31 @@ __device__ __forceinline__ uint64_t bytes_word(uint64_t r) {
   return acc;
 }
 
+// k-mer stream (distribution 9, the KMC3 workload of PAPER.md:280-282): record
+// i is the k-mer (k = 55 for 16-byte keys, 31 for 8-byte keys; 2 bits per base,
+// first base most significant) read at a uniform position of a pseudo-random
+// reference of KMER_L bases (circular); with probability 1/64 one base is
+// substituted (a "sequencing error": mostly singleton k-mers).
+constexpr uint64_t KMER_L = 1ull << 22;
+__device__ __forceinline__ uint64_t kmer_base(uint64_t seed, uint64_t x) {
+  return mix64(seed + 0x9E3779B97F4A7C15ull * (x + 0x100000000ull)) & 3ull;
+}
+__device__ void kmer_key(uint64_t seed, uint64_t i, int KW, uint64_t* key) {
+  const int k = KW == 2 ? 55 : 31;
+  const uint64_t p = uw(seed, i, 0, W_DEFAULT) % KMER_L, e = uw(seed, i, 1, W_DEFAULT);
+  const bool err = (e & 63ull) == 0;
+  const int epos = (int)((e >> 8) % (uint64_t)k);
+  uint64_t hi = 0, lo = 0;
+  for (int j = 0; j < k; ++j) {
+    uint64_t b = kmer_base(seed, (p + (uint64_t)j) % KMER_L);
+    if (err && j == epos) b = (b + 1ull + ((e >> 16) % 3ull)) & 3ull;
+    hi = (hi << 2) | (lo >> 62);
+    lo = (lo << 2) | b;
+  }
+  key[0] = lo;
+  key[1] = hi;
+}
+
 __global__ void k_generate(uint64_t* __restrict__ out, uint64_t n, uint64_t first, int RW, int KW,
                            int dist, int payload, uint64_t seed) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
@@ -86,6 +111,9 @@ __global__ void k_generate(uint64_t* __restrict__ out, uint64_t n, uint64_t firs
       }
       case 8:
         for (int kw = 0; kw < KW; ++kw) key[kw] = bytes_word(uw(seed, i, 4 + kw, W_DEFAULT));
+        break;
+      case 9:
+        kmer_key(seed, i, KW, key);
         break;
       default: {
         uint64_t k;

@@ -44,7 +44,9 @@ DISTS = {
     "few": 6,         # 7 distinct keys
     "consttop": 7,    # top 3 bytes fixed non-zero, rest uniform
     "bytes": 8,       # every key byte drawn from {0x00, 0x01, 0xFF}: ties at every digit
+    "kmer": 9,        # k-mers (k = 55 / 31) of a 2^22-base pseudo-random reference, 1/64 with one error
 }
+KMER_L = 1 << 22
 PAYLOADS = {"random": 0, "index": 1}
 
 # The five BASELINE.json configurations (seed = 170300687000 + config number).
@@ -55,6 +57,13 @@ CONFIGS = {
     "c4": dict(n=1_000_000_000, R=32, K=16, dist="uniform", payload="random", seed=170300687004),
     "c5": dict(n=1_000_000_000, R=8, K=8, dist="uniform", payload="random", seed=170300687005),
 }
+# The KMC3 consumer workload ("413 M 16 B-key
+# records"): a synthetic k-mer stream (the KMC set is not available), sorted then
+# run-length counted.  Not one of BASELINE.json's configs.
+EXTRA_CONFIGS = {
+    "kmc": dict(n=413_000_000, R=16, K=16, dist="kmer", payload="random", seed=170300687006),
+}
+CONFIGS.update(EXTRA_CONFIGS)
 
 
 def mix64(z):
@@ -153,6 +162,23 @@ def key_words(dist: str, seed: int, idx, K: int):
         k = mix64(u(seed, idx, 0) % np.uint64(7))
     elif d == 7:
         k = np.uint64(0xABCDEF << 40) | (u(seed, idx, 0) >> np.uint64(24))
+    elif d == 9:  # must match kmer_key in datagen.cu
+        k = 55 if nw == 2 else 31
+        p = u(seed, idx, 0) % np.uint64(KMER_L)
+        e = u(seed, idx, 1)
+        err = (e & np.uint64(63)) == 0
+        epos = (e >> np.uint64(8)) % np.uint64(k)
+        hi = np.zeros(idx.shape, dtype=np.uint64)
+        lo = np.zeros(idx.shape, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            for j in range(k):
+                x = (p + np.uint64(j)) % np.uint64(KMER_L)
+                b = mix64(np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + GOLDEN * (x + np.uint64(1 << 32))) & np.uint64(3)
+                sub = (b + np.uint64(1) + ((e >> np.uint64(16)) % np.uint64(3))) & np.uint64(3)
+                b = np.where(err & (epos == np.uint64(j)), sub, b)
+                hi = (hi << np.uint64(2)) | (lo >> np.uint64(62))
+                lo = (lo << np.uint64(2)) | b
+        return [lo] if nw == 1 else [lo, hi]
     elif d == 8:
         words = []
         for kw in range(nw):

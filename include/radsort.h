@@ -175,6 +175,18 @@ void radsort_finalize(void);
 /* Library version, e.g. "radsort 0.1 sm_100a". */
 const char* radsort_version(void);
 
+/* Run-length "unique key + count" over records sorted by radsort_sort (the
+ * k-mer counting step the paper's sorter serves in KMC3).
+ * dev_sorted: n records of rec_size bytes, non-decreasing keys (any built
+ * layout), n < 2^32.  Output, on the device: dev_keys_out[u] = the u-th
+ * distinct key (key_size bytes, same little-endian layout as in a record) and
+ * dev_counts_out[u] = its number of records, for u < *n_unique (host).  Both
+ * output buffers must hold n entries (the worst case).  Work is ordered on
+ * `stream`; the call returns after synchronizing it (to report *n_unique). */
+radsort_status radsort_unique_count(const void* dev_sorted, uint64_t n, uint32_t rec_size, uint32_t key_size,
+                                    void* dev_keys_out, uint32_t* dev_counts_out, uint64_t* n_unique,
+                                    cudaStream_t stream);
+
 /* Tiny-sorter benchmark (the GPU analog of PAPER.md:193-232 §4.1, Fig. 1;
  * benchmark infrastructure, not on the sort path): `bins` arrays of n
  * records (rec_size, key_size in {(8,8), (16,8), (16,16), (32,8), (32,16)}),

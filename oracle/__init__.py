@@ -13,8 +13,9 @@ passage it follows):
 - ``key_compare(a, b, K)``        -1 / 0 / +1
 - ``compare(got, want, K)``       canonical parity check (-1 = equal)
 - ``rank_bounds(records, K, key)`` (#keys < k, #keys <= k): sampled full-size checks
+- ``unique_count(sorted, K)``     distinct keys + counts (the KMC3 consumer)
 
 Pins: tests/test_oracle.py (brute force, numpy/lexsort special cases, SPEC
 worked examples in tests/golden/).  Parity pinned for every function above.
 """
-from .oracle import sort, digit, digit_hist, key_compare, compare, rank_bounds, lib_path, build  # noqa: F401
+from .oracle import sort, digit, digit_hist, key_compare, compare, rank_bounds, unique_count, lib_path, build  # noqa: F401

@@ -102,3 +102,20 @@ def rank_bounds(records: np.ndarray, K: int, key_record: np.ndarray):
     if _load().oracle_rank_bounds(a.ctypes.data, n, R, K, k.ctypes.data, ctypes.byref(lt), ctypes.byref(le)) != 0:
         raise ValueError("bad K/R")
     return int(lt.value), int(le.value)
+
+
+def unique_count(sorted_records: np.ndarray, K: int):
+    """Distinct keys of key-sorted records and their multiplicities, in key order
+    -- the k-mer counting step the paper's sorter serves in KMC3 (PAPER.md:280-282
+    §4.2).  Plain definition: a run of equal keys (bytes [0, K)) is one entry.
+    Returns (keys: (U, K) uint8, counts: (U,) int64).  Test infrastructure only."""
+    a = _as_records(sorted_records)
+    n = a.shape[0]
+    if n == 0:
+        return np.zeros((0, K), dtype=np.uint8), np.zeros((0,), dtype=np.int64)
+    keys = a[:, :K]
+    head = np.ones(n, dtype=bool)
+    head[1:] = np.any(keys[1:] != keys[:-1], axis=1)
+    starts = np.flatnonzero(head)
+    counts = np.diff(np.append(starts, n))
+    return np.ascontiguousarray(keys[starts]), counts.astype(np.int64)

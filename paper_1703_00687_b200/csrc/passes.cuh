@@ -974,7 +974,7 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
 }
 
 template <int R, int K, int IL, int LB>
-__global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
+__global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes, uint32_t cnt_bytes,
             uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
   extern __shared__ uint4 smem_raw[];

@@ -49,6 +49,22 @@ struct Sorter {
   // need 512 threads.
   static void launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
                            uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+    // small bins (up to 256 B of records per thread at 64 threads): 64-thread
+    // CTAs, so that many bins are in flight per SM (the per-bin phases are
+    // latency-bound)
+    constexpr int ILS = 256 / R >= 16 ? 16 : (256 / R >= 8 ? 8 : 4);
+    if (maxlen <= (uint32_t)(64 * ILS)) {
+      const uint32_t il = (maxlen + 63) / 64;
+#define RS_LOCAL_S(IL) launch_local_t<IL, 64>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms)
+      if (il <= 2) RS_LOCAL_S(2);
+      else if (il <= 4) RS_LOCAL_S(4);
+      else if constexpr (ILS >= 8) {
+        if (il <= 8) RS_LOCAL_S(8);
+        else if constexpr (ILS >= 16) RS_LOCAL_S(16);
+      }
+#undef RS_LOCAL_S
+      return;
+    }
     constexpr int ILMAX = (int)((C + 511) / 512);  // records per thread at 512 threads
     if ((size_t)maxlen > (size_t)256 * ILMAX) {
       launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms);

@@ -20,7 +20,8 @@ KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "mul
 EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
            "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
            "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
-           "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench"]
+           "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench",
+           "radsort_unique_count"]
 
 
 class Stats(ctypes.Structure):
@@ -71,10 +72,11 @@ def _load():
     L.radsort_plan_digit.argtypes = [vp, u64, ctypes.POINTER(u32)]
     L.radsort_plan_equal_split.argtypes = [vp, i32, u64, u64, vp]
     L.radsort_tinybench.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(ctypes.c_double)]
+    L.radsort_unique_count.argtypes = [vp, u64, u32, u32, vp, vp, ctypes.POINTER(u64), vp]
     for f in ("radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
               "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
               "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split",
-              "radsort_tinybench"):
+              "radsort_tinybench", "radsort_unique_count"):
         getattr(L, f).restype = i32
     return L
 
@@ -240,3 +242,18 @@ def tinybench(rec_size: int, key_size: int, n: int, algo: int, bins: int = 1 << 
     out = ctypes.c_double(0.0)
     _check(lib.radsort_tinybench(rec_size, key_size, n, algo, bins, ctypes.byref(out)))
     return out.value
+
+
+def unique_count(records, key_size: int, stream=None):
+    """Distinct keys and their counts of a sorted (n, R) uint8 CUDA tensor:
+    returns (keys: (U, key_size) uint8 tensor, counts: (U,) int32 tensor)."""
+    import torch
+
+    n, R = records.shape
+    keys = torch.empty((max(n, 1), key_size), dtype=torch.uint8, device=records.device)
+    counts = torch.empty((max(n, 1),), dtype=torch.int32, device=records.device)
+    out = ctypes.c_uint64(0)
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    _check(lib.radsort_unique_count(records.data_ptr(), n, R, key_size, keys.data_ptr(), counts.data_ptr(),
+                                    ctypes.byref(out), st))
+    return keys[:out.value], counts[:out.value]

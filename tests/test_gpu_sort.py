@@ -211,3 +211,29 @@ def test_tinybench_sorters_are_correct(R, K):
             if algo == 0 and n > 32:
                 continue
             assert rs.tinybench(R, K, n, algo, bins=4096) > 0.0
+
+
+@pytest.mark.parametrize("R,K", [(16, 16), (24, 8), (32, 16), (8, 8)])
+def test_kmer_sort_and_unique_count(R, K):
+    # NEXT-4, the KMC3 consumer: sort a k-mer stream, then run-length count it
+    # on the GPU; keys and counts must equal the oracle's
+    import paper_1703_00687_b200 as rs
+
+    for n in (1, 2, 4097, 300_001):
+        a = dg.generate(n, R, K, "kmer", payload="index" if R > K else "random", seed=n)
+        got = run_gpu_sort(a, K, guard=False)
+        assert oracle.compare(got, oracle.sort(a, K), K) == -1
+        t = torch.from_numpy(got.copy()).cuda()
+        keys, counts = rs.unique_count(t, K)
+        wk, wc = oracle.unique_count(got, K)
+        assert np.array_equal(keys.cpu().numpy(), wk)
+        assert np.array_equal(counts.cpu().numpy().astype(np.int64), wc)
+
+
+def test_kmer_device_generator_matches_host():
+    from datagen import device as dd
+
+    for R, K in ((16, 16), (8, 8)):
+        h = dg.generate(5000, R, K, "kmer", seed=3, first=77)
+        d = dd.generate_tensor(5000, R, K, "kmer", seed=3, first=77).cpu().numpy()
+        assert np.array_equal(h, d)

@@ -201,3 +201,63 @@ def test_rank_bounds_against_sorted_positions():
         assert lt == int(np.searchsorted(keys, keys[i], "left"))
         assert le == int(np.searchsorted(keys, keys[i], "right"))
         assert lt <= i < le
+
+
+def test_unique_count_pinned_to_counter():
+    # pinned to an independent method: collections.Counter over key bytes, on
+    # oracle-sorted tie-heavy inputs (every run found, counts exact, key order)
+    import collections
+
+    for K, R in ((8, 8), (8, 16), (16, 32)):
+        a = dg.generate(5000, R, K, "few" if K == 8 else "bytes", seed=5)
+        s = oracle.sort(a, K)
+        keys, counts = oracle.unique_count(s, K)
+        c = collections.Counter(bytes(r[:K]) for r in a)
+        assert len(keys) == len(c) and int(counts.sum()) == 5000
+        for k, m in zip(keys, counts):
+            assert c[bytes(k)] == m
+        # keys strictly increasing as K-byte little-endian integers
+        vals = [int.from_bytes(bytes(k), "little") for k in keys]
+        assert all(x < y for x, y in zip(vals, vals[1:]))
+    z = oracle.unique_count(np.zeros((0, 8), dtype=np.uint8), 8)
+    assert z[0].shape == (0, 8) and z[1].shape == (0,)
+
+
+def _kmer_reference(seed, idx, K):
+    # independent pure-Python restatement of the k-mer recipe (datagen "kmer")
+    mask = (1 << 64) - 1
+
+    def mix(z):
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9 & mask
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EB & mask
+        return z ^ (z >> 31)
+
+    def uw(i, w):
+        return mix((seed + (8 * i + w + 1) * 0x9E3779B97F4A7C15) & mask)
+
+    k = 55 if K == 16 else 31
+    L = 1 << 22
+    p, e = uw(idx, 0) % L, uw(idx, 1)
+    bases = [mix((seed + 0x9E3779B97F4A7C15 * ((p + j) % L + (1 << 32))) & mask) & 3 for j in range(k)]
+    if e & 63 == 0:
+        j = (e >> 8) % k
+        bases[j] = (bases[j] + 1 + ((e >> 16) % 3)) & 3
+    v = 0
+    for b in bases:
+        v = (v << 2) | b
+    return v
+
+
+def test_kmer_stream_matches_its_definition():
+    # the k-mer generator (KMC3 stand-in) against a pure-Python restatement:
+    # 2 bits per base, first base most significant, 1/64 records with one error
+    for K in (8, 16):
+        a = dg.generate(300, 16 if K == 8 else 32, K, "kmer", seed=11)
+        for i in (0, 1, 7, 63, 299):
+            got = int.from_bytes(bytes(a[i, :K]), "little")
+            assert got == _kmer_reference(11, i, K)
+        n_err = 0
+        b = dg.generate(20000, K, K, "kmer", seed=12)
+        # overlapping reads of a 2^22-base reference: some k-mers repeat
+        keys, counts = oracle.unique_count(oracle.sort(b, K), K)
+        assert counts.max() >= 1 and len(keys) <= 20000
