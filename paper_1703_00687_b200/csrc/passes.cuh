@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
         }
       }
     } else {  // a candidate for the dominant-key split: also count keys equal to / below the probe
-      constexpr int U2 = U / 4;
+      constexpr int U2 = U / 2;
       for (uint32_t i0 = tid; i0 < m; i0 += HIST_B * U2) {
         Key<K> k[U2];
 #pragma unroll
@@ -463,12 +463,13 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
 
 // One tile of a MODE_SPLIT segment (k_plan): three-way split around the
 // segment's dominant key -- class 0/1/2 = key below / equal to / above it.
-// Ranks by warp match + one smem atomic per class and warp; each class's range
+// Ranks by warp ballots + one smem atomic per class and warp; each class's range
 // is reserved per tile with one global atomic (order inside a class is free,
 // DESIGN.md R2).  The equal class is final: written to `records` (segment in
 // tmp), or skipped and filled later (segment in `records`, R == K).  Reads the
-// tile twice (L2 hits; rare tiles) and is kept out of line so the digit
-// scatter's register allocation does not pay for it.  Every thread calls it.
+// tile twice from L1/L2 (the scatter's register prefetch of the tile warms
+// them) and is kept out of line so the digit scatter's register allocation
+// does not pay for it.  Every thread calls it.
 template <int R, int K, int SB>
 __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base, uint32_t m, uint8_t* dst,
                                         uint8_t* recs, uint8_t* tmp, const uint32_t* __restrict__ segbase,
@@ -487,12 +488,17 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
       const Key<K> kx = ld_key<R, K>(src + (size_t)q * R);
       cl = key_lt(kx, probe) ? 0u : (key_eq(kx, probe) ? 1u : 2u);
     }
-    const uint32_t mk = __match_any_sync(0xffffffffu, cl);
-    const int leader = __ffs(mk) - 1;
+    const uint32_t m0 = __ballot_sync(0xffffffffu, cl == 0u), m1 = __ballot_sync(0xffffffffu, cl == 1u),
+                   m2 = __ballot_sync(0xffffffffu, cl == 2u);
     uint32_t b = 0;
-    if (lane == leader && cl < 3u) b = atomicAdd(&cnt[cl], (uint32_t)__popc(mk));
-    b = __shfl_sync(0xffffffffu, b, leader);
-    if (q < m) rkv[q] = (b + (uint32_t)__popc(mk & lanelt)) | (cl << 16);
+    if (lane < 3) {
+      const uint32_t mm = lane == 0 ? m0 : (lane == 1 ? m1 : m2);
+      if (mm) b = atomicAdd(&cnt[lane], (uint32_t)__popc(mm));
+    }
+    const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0), b1 = __shfl_sync(0xffffffffu, b, 1),
+                   b2 = __shfl_sync(0xffffffffu, b, 2);
+    const uint32_t mk = cl == 0u ? m0 : (cl == 1u ? m1 : m2);
+    if (q < m) rkv[q] = ((cl == 0u ? b0 : (cl == 1u ? b1 : b2)) + (uint32_t)__popc(mk & lanelt)) | (cl << 16);
   }
   __syncthreads();
   if (tid < 3) gofs[tid] = segbase[(size_t)s * RADIX + tid] + atomicAdd(&splitc[(size_t)s * 4 + tid], cnt[tid]);
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   // k+1 are in flight while tile k is looked back and written out)
   auto load = [&](uint32_t t, uint32_t s) {
     const Seg sg = segs[s];
-    if (sg.mode != MODE_SCATTER) return;
+    if (sg.mode != MODE_SCATTER && sg.mode != MODE_SPLIT) return;  // split tiles: a cache-warming prefetch
     const uint32_t lt = t - tile_start[s];
     const uint32_t m = min(T, sg.len - lt * T);
     const uint8_t* src = buf_of(sg.src, recs, tmp) + (size_t)(sg.off + lt * T) * R;

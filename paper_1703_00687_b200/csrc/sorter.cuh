@@ -278,6 +278,16 @@ struct Sorter {
         RS_CUDA(cudaGetLastError());
       }
       stats.levels = level + 1;
+      if (log && tm.on) {  // per-level kernel times (radsort_set_timing(1) + RADSORT_LOG=1)
+        float before[RADSORT_K_COUNT];
+        for (int q = 0; q < RADSORT_K_COUNT; ++q) before[q] = stats.kernel_ms[q];
+        tm.flush(stats);
+        fprintf(stderr, "[radsort] level %d ms: hist %.3f scatter %.3f children %.3f local %.3f\n", level,
+                stats.kernel_ms[RADSORT_K_HIST] - before[RADSORT_K_HIST],
+                stats.kernel_ms[RADSORT_K_SCATTER] - before[RADSORT_K_SCATTER],
+                stats.kernel_ms[RADSORT_K_CHILDREN] - before[RADSORT_K_CHILDREN],
+                stats.kernel_ms[RADSORT_K_LOCAL] - before[RADSORT_K_LOCAL]);
+      }
       tm.flush(stats);
       if (c.n_large_next == 0 && nloc == 0 && n_large == 0) break;
       n_large = c.n_large_next;
