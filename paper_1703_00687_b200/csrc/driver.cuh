@@ -40,6 +40,7 @@ struct Context {
   // workspace
   DevBuf large[2], local[2], hist, andor, segbase, tile_start, status, ctl, host_io[2];
   DevBuf splitc, probes;  // dominant-key split: per-segment class cursors; keys of the bins to fill
+  DevBuf tile_seg;        // tile -> segment map of the current level
   Ctl* h_ctl = nullptr;  // pinned
   uint32_t epoch = 0;
   cudaEvent_t ev[2 * 64] = {};

@@ -17,6 +17,17 @@ __device__ __forceinline__ uint32_t seg_of_tile(const uint32_t* __restrict__ til
   return lo;
 }
 
+// -------------------------------------------------------------- k_tilemap
+// tile -> segment map of the level (one independent binary search per tile,
+// all in parallel), so the histogram and scatter passes look a tile's segment
+// up with one load instead of a chain of dependent ones.
+static __global__ void k_tilemap(const uint32_t* __restrict__ tile_start, uint32_t nseg, const Ctl* __restrict__ ctl,
+                                 uint32_t* __restrict__ tile_seg) {
+  const uint32_t total = ctl->tiles_total;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x)
+    tile_seg[t] = seg_of_tile(tile_start, nseg, t);
+}
+
 // -------------------------------------------------------------- k_init
 // Level-0 set-up: the whole input is one bin.  If it fits the CTA-local
 // sorter it goes straight to the Local list, otherwise it becomes the single
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
                                                      uint32_t* __restrict__ hist, unsigned long long* __restrict__ andor,
                                                      const uint8_t* recs, const uint8_t* tmp, uint32_t* __restrict__ tile_pre,
                                                      uint32_t* __restrict__ ch_first, uint32_t* __restrict__ ch_last,
-                                                     uint32_t* __restrict__ ch_tot) {
+                                                     uint32_t* __restrict__ ch_tot, const uint32_t* __restrict__ tile_seg) {
   constexpr int KW = K / 8;
   constexpr int U = R <= 8 ? 16 : 8;  // keys in flight per thread
   __shared__ uint32_t h[RADIX], run[RADIX];
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
   uint64_t na[2] = {0, 0}, o[2] = {0, 0};
   uint32_t n_eq = 0, n_lt = 0;  // keys equal to / below the segment's probe key
   unsigned long long cnt_recs = 0;
-  uint32_t cur = seg_of_tile(tile_start, nseg, t0);
+  uint32_t cur = __ldg(tile_seg + t0);
   uint32_t cur_end = tile_start[cur + 1];
   Key<K> probe{};
   uint32_t probe_seg = NO_SEG;  // the probe (first record's key) is loaded once per segment
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
   for (uint32_t t = t0; t < t1; ++t) {
     if (t >= cur_end) {
       flush(cur);
-      cur = seg_of_tile(tile_start, nseg, t);
+      cur = __ldg(tile_seg + t);
       cur_end = tile_start[cur + 1];
     }
     const Seg sg = segs[cur];
@@ -526,7 +537,8 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
                                                        const uint32_t* __restrict__ ch_first,
                                                        const uint32_t* __restrict__ carry_in, uint32_t hist_grid,
                                                        uint32_t* __restrict__ splitc,
-                                                       const unsigned long long* __restrict__ probes) {
+                                                       const unsigned long long* __restrict__ probes,
+                                                       const uint32_t* __restrict__ tile_seg) {
   constexpr uint32_t T = tile_recs<R, TB, SB>();
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
@@ -548,7 +560,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   auto take = [&]() {
     const uint32_t t = atomicAdd(&ctl->scatter_ticket, 1u);
     sh_t = t;
-    sh_s = t < total ? seg_of_tile(tile_start, nseg, t) : 0u;
+    sh_s = t < total ? (tile_seg ? __ldg(tile_seg + t) : seg_of_tile(tile_start, nseg, t)) : 0u;
   };
   Rec<R> r[I];
   // issue this tile's loads into r[] (software pipelining: the loads of tile

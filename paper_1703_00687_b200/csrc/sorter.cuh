@@ -88,7 +88,7 @@ struct Sorter {
     Seg* Lo[2];
     uint32_t *hist, *segbase, *tile_start;
     unsigned long long *andor, *status, *probes;
-    uint32_t* splitc;
+    uint32_t *splitc, *tile_seg;
     Ctl* ctl;
     size_t tiles_max;
   };
@@ -108,6 +108,7 @@ struct Sorter {
     if ((rs = ensure(ctx->andor, capL * 8 * sizeof(unsigned long long)))) return rs;
     if ((rs = ensure(ctx->splitc, capL * 4 * sizeof(uint32_t)))) return rs;
     if ((rs = ensure(ctx->probes, capL * 2 * sizeof(unsigned long long)))) return rs;
+    if ((rs = ensure(ctx->tile_seg, tiles_max * sizeof(uint32_t)))) return rs;
     if ((rs = ensure(ctx->tile_start, (capL + 1) * sizeof(uint32_t)))) return rs;
     const size_t old_status = ctx->status.bytes;
     if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
@@ -123,6 +124,7 @@ struct Sorter {
     v.andor = (unsigned long long*)ctx->andor.p;
     v.splitc = (uint32_t*)ctx->splitc.p;
     v.probes = (unsigned long long*)ctx->probes.p;
+    v.tile_seg = (uint32_t*)ctx->tile_seg.p;
     v.tile_start = (uint32_t*)ctx->tile_start.p;
     v.status = (unsigned long long*)ctx->status.p;
     v.ctl = (Ctl*)ctx->ctl.p;
@@ -217,14 +219,16 @@ struct Sorter {
         RS_CUDA(cudaMemsetAsync(andor, 0, (size_t)n_large * 8 * sizeof(unsigned long long), st));
         tm.begin(RADSORT_K_PLAN);
         k_prep<<<1, 1024, 0, st>>>(L[cur], n_large, T, tile_start, ctl, nxt);
-        tm.end();
         const size_t tiles_ub = std::min(tiles_max, (size_t)n / T + n_large + 1);
+        k_tilemap<<<(unsigned)std::min<size_t>((tiles_ub + 255) / 256, (size_t)ctx->sms * 16), 256, 0, st>>>(
+            tile_start, n_large, ctl, v.tile_seg);
+        tm.end();
         const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
         tm.begin(RADSORT_K_HIST);
         if (pre) {
           k_cand<R, K><<<(n_large + 7) / 8, 256, 0, st>>>(L[cur], n_large, recs, tmp);
           k_hist_pre<R, K, T><<<hist_grid, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp,
-                                                             tile_pre, ch_first, ch_last, ch_tot);
+                                                             tile_pre, ch_first, ch_last, ch_tot, v.tile_seg);
           k_carry<<<1, RADIX, 0, st>>>(ch_first, ch_last, ch_tot, hist_grid, carry_in);
         } else {
           k_hist<R, K, T><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
@@ -242,11 +246,11 @@ struct Sorter {
         if (pre)
           k_scatter<R, K, TB, SB, MINB, true><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
                                                                   ctx->epoch, ctl, recs, tmp, tile_pre, ch_first,
-                                                                  carry_in, hist_grid, v.splitc, v.probes);
+                                                                  carry_in, hist_grid, v.splitc, v.probes, v.tile_seg);
         else
           k_scatter<R, K, TB, SB, MINB, false><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
                                                                    ctx->epoch, ctl, recs, tmp, nullptr, nullptr,
-                                                                   nullptr, 0, v.splitc, v.probes);
+                                                                   nullptr, 0, v.splitc, v.probes, v.tile_seg);
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
@@ -396,7 +400,7 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   const unsigned gs = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_s));
   k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false><<<gs, MULTI_SB, MULTI_TB, st>>>(
       v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, nullptr, nullptr, nullptr, 0,
-      v.splitc, v.probes);
+      v.splitc, v.probes, nullptr);
   RS_CUDA(cudaGetLastError());
   RS_CUDA(cudaStreamSynchronize(st));
   workspace_release(ctx, st);
