@@ -804,6 +804,13 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
     const uint32_t off = coff[v], len = clen[v];
     const uint8_t* src = cbuf + (size_t)off * R;
     uint8_t* out = recs + (size_t)off * R;
+    {  // the warp's next bin into L1 while this one is sorted (one 128-byte line per lane)
+      const int vn = v + CHILD_B / 32;
+      if (vn < RADIX && (cls[vn] == C_TINY || cls[vn] == C_ES)) {
+        const uint8_t* pn = cbuf + (size_t)coff[vn] * R + (size_t)lane * 128;
+        if ((uint32_t)lane * 128u < clen[vn] * (uint32_t)R) asm volatile("prefetch.global.L1 [%0];" ::"l"(pn));
+      }
+    }
     if (c == C_COPY) {
       warp_copy<R>(src, out, len, lane);
     } else if (c == C_ES) {
