@@ -372,13 +372,13 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
 
 // -------------------------------------------------------------- k_carry
 // Carry of each chunk's first segment from the earlier chunks: a segmented
-// scan over the chunks, one thread per digit (single CTA; 16 chunks in flight).
+// scan over the chunks, one thread per digit (single CTA; 32 chunks in flight).
 static __global__ void __launch_bounds__(RADIX) k_carry(const uint32_t* __restrict__ ch_first, const uint32_t* __restrict__ ch_last,
                                                  const uint32_t* __restrict__ ch_tot, uint32_t nch,
                                                  uint32_t* __restrict__ carry_in) {
   const int d = threadIdx.x;
   uint32_t carry = 0, prev_last = NO_SEG;
-  constexpr int B = 16;
+  constexpr int B = 32;
   for (uint32_t c0 = 0; c0 < nch; c0 += B) {
     uint32_t f[B], l[B], tt[B];
 #pragma unroll
