@@ -113,8 +113,14 @@ template <int R, int K>
 radsort_status multi_bounds(Context* ctx, const uint8_t* buf, const uint32_t* lo, const uint32_t* hi,
                             const uint64_t* probes, uint32_t M, cudaStream_t st, uint64_t* lt, uint64_t* le);
 
+template <int R, int K>
+radsort_status run_layout_segs(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, const uint32_t* off,
+                               const uint32_t* len, uint32_t nseg, uint32_t depth, cudaStream_t st, radsort_stats& s);
+
 struct LayoutOps {
   radsort_status (*sort)(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
+  radsort_status (*sort_segs)(Context*, uint8_t*, uint8_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t,
+                              uint32_t, cudaStream_t, radsort_stats&);
   radsort_status (*hist)(Context*, const uint8_t*, uint32_t, uint32_t, cudaStream_t, uint64_t*, uint64_t*);
   radsort_status (*scatter)(Context*, uint8_t*, uint8_t*, uint32_t, uint32_t, const uint64_t*, cudaStream_t);
   radsort_status (*bounds)(Context*, const uint8_t*, const uint32_t*, const uint32_t*, const uint64_t*, uint32_t,

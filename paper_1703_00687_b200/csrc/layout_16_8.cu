@@ -2,6 +2,8 @@
 // rec_size=16, key_size=8.
 #include "sorter.cuh"
 namespace radsort {
+template radsort_status run_layout_segs<16, 8>(Context*, uint8_t*, uint8_t*, uint32_t, const uint32_t*,
+                                                  const uint32_t*, uint32_t, uint32_t, cudaStream_t, radsort_stats&);
 template radsort_status run_layout<16, 8>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
 template radsort_status multi_hist<16, 8>(Context*, const uint8_t*, uint32_t, uint32_t, cudaStream_t, uint64_t*,
                                            uint64_t*);

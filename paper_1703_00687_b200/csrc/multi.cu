@@ -15,9 +15,12 @@
 //     count stays <= Q_g
 //  5. records equal to k_g are split across ranks by source-rank order so the
 //     quotas hold exactly (any order inside an equal-key run is correct, R2)
-//  6. send ranges are contiguous slices of tmp; counts allgathered; grouped
-//     ncclSend/ncclRecv move them into dev_records (NVLink / NVSwitch)
-//  7. the received shard is sorted by the single-GPU path.
+//  6. send ranges are contiguous slices of tmp, grouped by d0; they travel as
+//     one message per (destination, d0 bucket) in grouped ncclSend/ncclRecv
+//     (NVLink / NVSwitch), so that each receiver lands its records bucket by
+//     bucket (bucket b from every sender contiguous in dev_records)
+//  7. the received shard is sorted by the single-GPU path, starting from those
+//     buckets at digit d0 + 1: the receiver never re-partitions by d0.
 //
 // The algorithm is written against a small Transport interface with two
 // implementations: NCCL (the product) and an in-process loopback with host
@@ -57,6 +60,14 @@ static void plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, u
 // -------------------------------------------------------------- transport
 enum class ROp { Sum, Min, Max };
 
+// one point-to-point message of the exchange: `bytes` bytes at byte offset
+// `off` of the send (or receive) buffer, to (or from) rank `peer`; messages
+// between one pair of ranks match in the order they are listed
+struct Msg {
+  int peer;
+  uint64_t off, bytes;
+};
+
 struct Transport {
   virtual ~Transport() {}
   virtual int rank() const = 0;
@@ -64,11 +75,9 @@ struct Transport {
   // host in -> host out (small control data)
   virtual radsort_status allreduce(const uint64_t* in, uint64_t* out, size_t cnt, ROp op, cudaStream_t st) = 0;
   virtual radsort_status allgather(const uint64_t* in, uint64_t* out, size_t cnt, cudaStream_t st) = 0;
-  // device data: send_bytes[p] bytes from send + send_off[p] to rank p, receive
-  // recv_bytes[p] bytes from rank p at recv + recv_off[p]
-  virtual radsort_status alltoallv(const uint8_t* send, const uint64_t* send_off, const uint64_t* send_bytes,
-                                   uint8_t* recv, const uint64_t* recv_off, const uint64_t* recv_bytes,
-                                   cudaStream_t st) = 0;
+  // device data: every message of `sends` from `send`, every one of `recvs` into `recv`
+  virtual radsort_status exchange(const uint8_t* send, const std::vector<Msg>& sends, uint8_t* recv,
+                                  const std::vector<Msg>& recvs, cudaStream_t st) = 0;
 };
 
 #define RS_NCCL(x)                                                                             \
@@ -122,13 +131,11 @@ struct NcclTransport : Transport {
     RS_CUDA(cudaMemcpyAsync(out, d + cnt, (size_t)g * cnt * 8, cudaMemcpyDeviceToHost, st));
     return check(st);
   }
-  radsort_status alltoallv(const uint8_t* send, const uint64_t* send_off, const uint64_t* send_bytes, uint8_t* recv,
-                           const uint64_t* recv_off, const uint64_t* recv_bytes, cudaStream_t st) override {
+  radsort_status exchange(const uint8_t* send, const std::vector<Msg>& sends, uint8_t* recv,
+                          const std::vector<Msg>& recvs, cudaStream_t st) override {
     RS_NCCL(ncclGroupStart());
-    for (int p = 0; p < g; ++p) {
-      if (send_bytes[p]) RS_NCCL(ncclSend(send + send_off[p], send_bytes[p], ncclUint8, p, comm, st));
-      if (recv_bytes[p]) RS_NCCL(ncclRecv(recv + recv_off[p], recv_bytes[p], ncclUint8, p, comm, st));
-    }
+    for (const Msg& m : sends) RS_NCCL(ncclSend(send + m.off, m.bytes, ncclUint8, m.peer, comm, st));
+    for (const Msg& m : recvs) RS_NCCL(ncclRecv(recv + m.off, m.bytes, ncclUint8, m.peer, comm, st));
     RS_NCCL(ncclGroupEnd());
     return check(st);
   }
@@ -143,8 +150,8 @@ struct LoopGroup {
   uint64_t gen = 0;
   std::vector<std::vector<uint64_t>> slot;
   std::vector<const uint8_t*> sbase;
-  std::vector<std::vector<uint64_t>> soff, sbytes;
-  explicit LoopGroup(int g) : G(g), slot(g), sbase(g), soff(g), sbytes(g) {}
+  std::vector<std::vector<Msg>> sends;
+  explicit LoopGroup(int g) : G(g), slot(g), sbase(g), sends(g) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const uint64_t my = gen;
@@ -185,26 +192,37 @@ struct LoopTransport : Transport {
     grp->barrier();
     return RADSORT_OK;
   }
-  radsort_status alltoallv(const uint8_t* send, const uint64_t* send_off, const uint64_t* send_bytes, uint8_t* recv,
-                           const uint64_t* recv_off, const uint64_t* recv_bytes, cudaStream_t st) override {
+  radsort_status exchange(const uint8_t* send, const std::vector<Msg>& sends, uint8_t* recv,
+                          const std::vector<Msg>& recvs, cudaStream_t st) override {
     grp->sbase[r] = send;
-    grp->soff[r].assign(send_off, send_off + grp->G);
-    grp->sbytes[r].assign(send_bytes, send_bytes + grp->G);
+    grp->sends[r] = sends;
     RS_CUDA(cudaStreamSynchronize(st));  // every rank's send data is complete before peers read it
     grp->barrier();
-    for (int p = 0; p < grp->G; ++p) {
-      const uint64_t b = grp->sbytes[p][r];
-      if (b != recv_bytes[p]) {
-        set_detail("loopback: rank %d expects %llu bytes from %d, sender has %llu", r,
-                   (unsigned long long)recv_bytes[p], p, (unsigned long long)b);
-        grp->barrier();
-        return RADSORT_ERR_INVALID_ARG;
+    // the k-th message from p to r pairs with the k-th receive r lists from p
+    std::vector<size_t> cursor(grp->G, 0);
+    radsort_status rs = RADSORT_OK;
+    for (const Msg& m : recvs) {
+      const std::vector<Msg>& ps = grp->sends[m.peer];
+      size_t& k = cursor[m.peer];
+      while (k < ps.size() && ps[k].peer != r) ++k;
+      if (k == ps.size() || ps[k].bytes != m.bytes) {
+        set_detail("loopback: rank %d expects a %llu-byte message from %d that was not sent", r,
+                   (unsigned long long)m.bytes, m.peer);
+        rs = RADSORT_ERR_INVALID_ARG;
+        break;
       }
-      if (b) RS_CUDA(cudaMemcpyAsync(recv + recv_off[p], grp->sbase[p] + grp->soff[p][r], b, cudaMemcpyDeviceToDevice, st));
+      if (m.bytes)
+        if (cudaMemcpyAsync(recv + m.off, grp->sbase[m.peer] + ps[k].off, m.bytes, cudaMemcpyDeviceToDevice, st) !=
+            cudaSuccess) {
+          set_detail("loopback: cudaMemcpyAsync failed");
+          rs = RADSORT_ERR_CUDA;
+          break;
+        }
+      ++k;
     }
-    RS_CUDA(cudaStreamSynchronize(st));
+    if (cudaStreamSynchronize(st) != cudaSuccess && rs == RADSORT_OK) rs = RADSORT_ERR_CUDA;
     grp->barrier();
-    return RADSORT_OK;
+    return rs;
   }
 };
 
@@ -395,32 +413,57 @@ static radsort_status sort_multi_impl(Transport& tr, uint8_t* recs, uint8_t* tmp
   }
   for (int g = 1; g <= G; ++g) cut[g] = std::max(cut[g], cut[g - 1]);
 
-  // 6. exchange
+  // 6. exchange.  Each destination's records are contiguous in tmp and grouped
+  // by their top digit d0 (step 3); they go out as one message per bucket so
+  // that every receiver lands its records bucket by bucket (bucket b from all
+  // senders contiguous) and can start its MSD at digit d0 + 1 (step 7).
   std::vector<uint64_t> sc(G), S((size_t)G * G);
   for (int g = 0; g < G; ++g) sc[g] = cut[g + 1] - cut[g];
   if ((rs = tr.allgather(sc.data(), S.data(), G, st))) return rs;
-  std::vector<uint64_t> soff(G), sbytes(G), roff(G), rbytes(G);
+  std::vector<uint64_t> allh((size_t)G * 256), allcut((size_t)G * (G + 1));
+  if ((rs = tr.allgather(h, allh.data(), 256, st))) return rs;
+  if ((rs = tr.allgather(cut.data(), allcut.data(), (size_t)G + 1, st))) return rs;
+  std::vector<Msg> sends, recvs;
+  for (int p = 0; p < G; ++p)
+    for (int b = 0; b < 256; ++b) {
+      const uint64_t lo = std::max(cut[p], lbase[b]), hi = std::min(cut[p + 1], lbase[b + 1]);
+      if (hi > lo) sends.push_back({p, lo * R, (hi - lo) * R});
+    }
+  std::vector<uint32_t> seg_off, seg_len;
   uint64_t got = 0;
-  for (int p = 0; p < G; ++p) {
-    soff[p] = cut[p] * R;
-    sbytes[p] = sc[p] * R;
-    roff[p] = got * R;
-    rbytes[p] = S[(size_t)p * G + me] * R;
-    got += S[(size_t)p * G + me];
+  for (int b = 0; b < 256; ++b) {
+    const uint64_t b0 = got;
+    for (int r = 0; r < G; ++r) {
+      const uint64_t* hr = &allh[(size_t)r * 256];
+      uint64_t rb = 0;  // start of bucket b on rank r
+      for (int u = 0; u < b; ++u) rb += hr[u];
+      const uint64_t* cr = &allcut[(size_t)r * (G + 1)];
+      const uint64_t lo = std::max(cr[me], rb), hi = std::min(cr[me + 1], rb + hr[b]);
+      if (hi > lo) {
+        recvs.push_back({r, got * R, (hi - lo) * R});
+        got += hi - lo;
+      }
+    }
+    if (got > b0) {
+      seg_off.push_back((uint32_t)b0);
+      seg_len.push_back((uint32_t)(got - b0));
+    }
   }
   if (got != q[me]) {
     set_detail("exchange plan gives %llu records, quota %llu", (unsigned long long)got, (unsigned long long)q[me]);
     return RADSORT_ERR_CUDA;
   }
-  if ((rs = tr.alltoallv(tmp, soff.data(), sbytes.data(), recs, roff.data(), rbytes.data(), st))) return rs;
+  if ((rs = tr.exchange(tmp, sends, recs, recvs, st))) return rs;
   stats.nvlink_bytes_sent = (n_local - sc[me]) * R;
   stats.nvlink_bytes_recv = (got - S[(size_t)me * G + me]) * R;
 
-  // 7. local sort of the received key range
+  // 7. local sort of the received key range, from its top-digit buckets on
   radsort_stats sub = {};
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    if ((rs = ops->sort(ctx, recs, tmp, (uint32_t)got, st, sub))) return rs;
+    if ((rs = ops->sort_segs(ctx, recs, tmp, (uint32_t)got, seg_off.data(), seg_len.data(), (uint32_t)seg_off.size(),
+                             d0 + 1, st, sub)))
+      return rs;
   }
   stats.levels = sub.levels;
   stats.scatter_passes = sub.scatter_passes + 1;

@@ -39,7 +39,8 @@ Context* get_or_create_ctx(int dev) {
 
 const LayoutOps* layout_ops(uint32_t R, uint32_t K) {
 #define RS_OPS(r, k) \
-  static const LayoutOps ops_##r##_##k = {run_layout<r, k>, multi_hist<r, k>, multi_scatter<r, k>, multi_bounds<r, k>}
+  static const LayoutOps ops_##r##_##k = {run_layout<r, k>, run_layout_segs<r, k>, multi_hist<r, k>, \
+                                          multi_scatter<r, k>, multi_bounds<r, k>}
   RS_OPS(8, 8);
   RS_OPS(16, 8);
   RS_OPS(16, 16);

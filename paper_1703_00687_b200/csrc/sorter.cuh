@@ -134,22 +134,30 @@ struct Sorter {
 
   // Scatter/histogram tile configuration: TB bytes per tile, SB threads per
   // scatter CTA, MINB scatter CTAs per SM (RADSORT_SCATTER_CFG selects).
+  // Initial bins (multi-GPU receive side): records [off[i], off[i]+len[i]) of
+  // `recs` already share their first `depth` digits; nullptr = the whole array.
+  struct Init {
+    const uint32_t* off;
+    const uint32_t* len;
+    uint32_t nseg, depth;
+  };
+
   static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
-                            radsort_stats& stats) {
+                            radsort_stats& stats, const Init* init = nullptr) {
     const char* e = getenv("RADSORT_SCATTER_CFG");
     const int cfg = e ? atoi(e) : 1;
     switch (cfg) {
-      case 0: return run_cfg<65536, 512, 2>(ctx, recs, tmp, n, st, stats);
-      case 2: return run_cfg<32768, 512, 2>(ctx, recs, tmp, n, st, stats);
-      case 3: return run_cfg<16384, 256, 4>(ctx, recs, tmp, n, st, stats);
-      case 4: return run_cfg<49152, 384, 3>(ctx, recs, tmp, n, st, stats);
-      default: return run_cfg<32768, 256, 4>(ctx, recs, tmp, n, st, stats);  // measured best
+      case 0: return run_cfg<65536, 512, 2>(ctx, recs, tmp, n, st, stats, init);
+      case 2: return run_cfg<32768, 512, 2>(ctx, recs, tmp, n, st, stats, init);
+      case 3: return run_cfg<16384, 256, 4>(ctx, recs, tmp, n, st, stats, init);
+      case 4: return run_cfg<49152, 384, 3>(ctx, recs, tmp, n, st, stats, init);
+      default: return run_cfg<32768, 256, 4>(ctx, recs, tmp, n, st, stats, init);  // measured best
     }
   }
 
   template <int TB, int SB, int MINB>
   static radsort_status run_cfg(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
-                                radsort_stats& stats) {
+                                radsort_stats& stats, const Init* init) {
     constexpr uint32_t T = tile_recs<R, TB, SB>();
     set_attrs();
     static bool attr = false;
@@ -198,9 +206,32 @@ struct Sorter {
     Timer tm(ctx, st);
     const bool log = getenv("RADSORT_LOG") && getenv("RADSORT_LOG")[0] == '1';
 
-    k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
-    uint32_t n_large = n > C ? 1u : 0u;
-    if (n_large) {
+    uint32_t n_large;
+    if (init) {  // presegmented input: the bins go straight to the Large / Local lists
+      std::vector<Seg> lg, lc;
+      Ctl c0 = {};
+      for (uint32_t i = 0; i < init->nseg && init->depth < (uint32_t)K; ++i) {
+        if (init->len[i] < 2) continue;
+        const Seg sg = {init->off[i], init->len[i], (uint8_t)init->depth, SRC_REC, MODE_NONE, 0, 0};
+        if (init->len[i] > C) {
+          lg.push_back(sg);
+        } else {
+          lc.push_back(sg);
+          c0.max_local_len[0] = std::max(c0.max_local_len[0], init->len[i]);
+        }
+      }
+      c0.n_local[0] = (uint32_t)lc.size();
+      c0.d0 = init->depth;
+      if (!lg.empty()) RS_CUDA(cudaMemcpyAsync(L[0], lg.data(), lg.size() * sizeof(Seg), cudaMemcpyHostToDevice, st));
+      if (!lc.empty()) RS_CUDA(cudaMemcpyAsync(Lo[0], lc.data(), lc.size() * sizeof(Seg), cudaMemcpyHostToDevice, st));
+      RS_CUDA(cudaMemcpyAsync(ctl, &c0, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+      RS_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+      n_large = (uint32_t)lg.size();
+    } else {
+      k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
+      n_large = n > C ? 1u : 0u;
+    }
+    if (n_large && !init) {
       tm.begin(RADSORT_K_SAMPLE);
       k_sample<R, K><<<1, 256, 0, st>>>(L[0], ctl, recs, n);
       tm.end();
@@ -330,6 +361,18 @@ template <int R, int K>
 radsort_status run_layout(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st, radsort_stats& s) {
   workspace_acquire(ctx, st);
   const radsort_status rs = Sorter<R, K>::run(ctx, recs, tmp, n, st, s);
+  workspace_release(ctx, st);
+  return rs;
+}
+
+// The same sort started from bins that already share their first `depth`
+// digits (the multi-GPU receive side: data arrives grouped by its top digit).
+template <int R, int K>
+radsort_status run_layout_segs(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, const uint32_t* off,
+                               const uint32_t* len, uint32_t nseg, uint32_t depth, cudaStream_t st, radsort_stats& s) {
+  workspace_acquire(ctx, st);
+  const typename Sorter<R, K>::Init init = {off, len, nseg, depth};
+  const radsort_status rs = Sorter<R, K>::run(ctx, recs, tmp, n, st, s, &init);
   workspace_release(ctx, st);
   return rs;
 }
