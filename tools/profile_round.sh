@@ -9,14 +9,20 @@ mkdir -p gpurun_out/prof
 O=gpurun_out/prof
 : > $O/bench_all.jsonl
 timeout 600 python bench.py --steps 5 --warmup 3 >> $O/bench_all.jsonl 2> $O/bench_c2.err
-for c in c1 c3 c4 c5; do
+for c in c1 c3 c4 c5 kmc; do
   timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline >> $O/bench_all.jsonl 2> $O/bench_$c.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2> $O/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/c2_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
-for c in c2 c5 c3; do
+for c in c2 c5; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_local|k_hist_pre" -c 5 \
     -o $O/${c}_full python bench.py --config $c --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_$c.log 2>&1
+done
+# DRAM bytes per launch only (small reports; the gpurun return limit is 64 MiB)
+for c in c3 c4; do
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:"k_scatter|k_local|k_hist_pre" -c 8 \
+    -o $O/${c}_dram python bench.py --config $c --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_$c.log 2>&1
 done
 ls -la $O
