@@ -23,6 +23,7 @@ CSRC = os.path.join(PKG, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
+CUFLAGS += os.environ.get("RADSORT_NVCC_EXTRA", "").split()  # e.g. -DRADSORT_PHASE_PROF (profiling builds)
 
 
 def _nccl_dirs():

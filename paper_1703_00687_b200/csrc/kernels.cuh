@@ -9,6 +9,7 @@
 //
 // Shares no code with oracle/ or datagen/.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>

@@ -734,7 +734,7 @@ template <int R, int K>
 __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
                                                       Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
-                                                      unsigned long long* __restrict__ probes) {
+                                                      unsigned long long* __restrict__ probes, uint32_t lcap) {
   enum : uint8_t { C_NONE = 0, C_COPY = 1, C_ES = 2, C_TINY = 3 };
   extern __shared__ uint4 smem_raw[];
   __shared__ uint8_t cls[RADIX];
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
       c = C_ES;
     } else if (len <= TINY_MAX) {
       c = C_TINY;
-    } else if (len <= C) {
+    } else if (len <= lcap) {  // CTA-local sort (<= C) or cluster-local sort (<= lcap)
       Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
       local_cur[atomicAdd(&ctl->n_local[cur], 1u)] = ns;
       atomicMax(&ctl->max_local_len[cur], len);
@@ -947,11 +947,18 @@ template <int R, int K, int LB, int NTW>
 __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* start16, uint32_t* blist, uint32_t cap,
                                              uint32_t n, uint32_t nbk, uint32_t d, uint32_t W, uint32_t ncol,
                                              uint32_t* s_nbig, TailScratch<K>* tsc, uint8_t* out, uint32_t off,
-                                             Seg* local_next, int nxt, Ctl* ctl) {
+                                             Seg* local_next, int nxt, Ctl* ctl, bool bulk = false,
+                                             unsigned long long* pfx = nullptr) {
   constexpr int NW = LB / 32;
   constexpr uint32_t ES = es_max<R>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto start_of = [&](uint32_t b) { return (uint32_t)start16[b]; };
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long fA = clock64();
+#define RS_FPROF(i) do { if (pfx && tid == 0) { const unsigned long long fB = clock64(); pfx[i] += fB - fA; fA = fB; } } while (0)
+#else
+#define RS_FPROF(i) do { } while (0)
+#endif
   uint32_t nbig = 0;
   if (ncol) {
     for (uint32_t e = tid; e < ncol; e += LB) {
@@ -968,6 +975,7 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
       }
     }
     __syncthreads();
+    RS_FPROF(0);
     nbig = *s_nbig;
     for (uint32_t e = warp; e < nbig; e += NW) {  // > ES records: one key or several?
       const uint32_t en = blist[cap - 1u - e];
@@ -979,8 +987,26 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
     }
     if (nbig) __syncthreads();
   }
-  for (uint32_t q = tid; q < n; q += LB) st_rec<R>(out + (size_t)q * R, ld_rec<R>(stage + (size_t)q * R));
+  RS_FPROF(1);
+  if (bulk) {  // one TMA bulk store (out and n * R 16-byte aligned); the caller waits before reusing the stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out), "r"(sa), "r"(n * (uint32_t)R)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  } else {
+    for (uint32_t q = tid; q < n; q += LB) st_rec<R>(out + (size_t)q * R, ld_rec<R>(stage + (size_t)q * R));
+  }
+#ifdef RADSORT_PHASE_PROF
+  __syncthreads();
+#endif
+  RS_FPROF(2);
+#undef RS_FPROF
   if (!nbig) return false;
+  if (bulk && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // tails overwrite their part
   __syncthreads();  // written out; counters dead: the tail sorter's scratch aliases them
   const uint32_t nd = d + (W >= 16 ? 2u : 1u);  // digits shared by a bucket's keys
   for (uint32_t e = warp; e < nbig && warp < NTW; e += NTW) {
@@ -1012,7 +1038,9 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
   __shared__ uint32_t wsum[NW], s_ncol, s_nbig, s_const;
   __shared__ unsigned long long sna[2], so[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t C = local_capacity<R>();  // larger bins of the list belong to k_local_cluster
   uint32_t bi = blockIdx.x;
+  while (bi < nlist && list[bi].len > C) bi += gridDim.x;
   if (bi >= nlist) return;
   auto zero_cnt = [&](uint32_t bytes) {
     uint4* c4 = reinterpret_cast<uint4*>(cnt);
@@ -1147,7 +1175,8 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     }
     // registers are free: the next bin's loads overlap this bin's write-out;
     // the bin after next streams into L2
-    const uint32_t nb = bi + gridDim.x;
+    uint32_t nb = bi + gridDim.x;
+    while (nb < nlist && list[nb].len > C) nb += gridDim.x;
     Seg nsg = sg;
     if (nb < nlist) {
       nsg = list[nb];
@@ -1179,6 +1208,297 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
   }
 #endif
 #undef RS_PROF
+}
+
+// -------------------------------------------------------------- k_local_cluster
+// The CTA-local sort for bins larger than one CTA's capacity C (up to about
+// CS * C): a cluster of CS CTAs sorts one bin (GPU analog of PAPER.md:134, the
+// counting scatter of a bin that fits on chip, with the cluster's distributed
+// shared memory as the chip).  The composite digit's 2^W buckets are split
+// into CS slices; CTA o owns slice o and sorts the records that fall in it.
+//   1 each CTA loads 1/CS of the bin and ranks its records in a private
+//     counter array over all 2^W buckets (local atomics);
+//   2 the owner of each slice sums the CS counter arrays over its slice
+//     (coalesced DSMEM reads), scans them into the slice's bucket starts,
+//     lists the buckets of >= 2 records, and writes each CTA's base offset
+//     per bucket back into that CTA's array (coalesced DSMEM writes);
+//   3 every record is stored once into its owner's staging buffer, at
+//     base (local read) + rank -- one remote store per record;
+//   4 each CTA finishes its slice exactly as k_local does (fix-up of
+//     colliding buckets, coalesced write-out).
+// A bin whose slice would overflow a CTA's staging buffer, or whose composite
+// digit is constant, is handed to the next level as a Large bin (nothing has
+// been written yet).  The next bin of each CTA is prefetched into L2 (TMA
+// bulk prefetch) while the current one is sorted.
+template <int R, int K, int IL, int LB, int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
+    k_local_cluster(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes,
+                    uint32_t cnt_bytes, uint32_t cap, Seg* local_next, int nxt, Seg* large_next, Ctl* ctl,
+                    uint8_t* recs, uint8_t* tmp) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ uint4 smem_raw[];
+  constexpr int NW = LB / 32;
+  constexpr uint32_t LCS = CS == 2 ? 1u : (CS == 4 ? 2u : 3u);  // log2 CS
+  constexpr uint32_t WMIN = LCS + 3u + 9u;                         // >= one 8-bucket chunk per thread and slice
+  constexpr int NTW = (int)((2u << WMIN) / sizeof(TailScratch<K>)) < NW ? (int)((2u << WMIN) / sizeof(TailScratch<K>))
+                                                                           : NW;  // tail scratch aliases the counters
+  constexpr uint32_t C = local_capacity<R>();
+  uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(stage + stage_bytes);  // 2^W u16: counts, then bases
+  uint32_t* sst = cnt + cnt_bytes / 4u;                              // the slice's bucket starts (u16)
+  uint32_t* blist = sst + (cnt_bytes >> LCS) / 4u;
+  const uint16_t* cnt16 = reinterpret_cast<const uint16_t*>(cnt);
+  __shared__ uint32_t wsum[NW], s_ncol, s_nbig, s_tot[CS], s_np, s_n3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t crank = cl.block_rank();
+  const uint32_t ncl = gridDim.x / CS;
+  const uint32_t stage_cap = stage_bytes / R;
+  auto zero_cnt = [&](uint32_t bytes) {
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (uint32_t i = tid; i < bytes / 16u; i += LB) c4[i] = make_uint4(0, 0, 0, 0);
+  };
+  auto prefetch_l2 = [&](uint32_t b) {  // this CTA's part of bin b
+    if (tid == 0 && b < nlist) {
+      const Seg g = list[b];
+      if (g.len <= C) return;
+      const uint32_t pt = (g.len + CS - 1) / CS, q0 = min(g.len, crank * pt), qn = min(g.len, q0 + pt) - q0;
+      const uintptr_t s0 = (uintptr_t)(buf_of(g.src, recs, tmp) + ((size_t)g.off + q0) * R);
+      const uintptr_t s1 = (s0 + 15) & ~(uintptr_t)15, e1 = (s0 + (size_t)qn * R) & ~(uintptr_t)15;
+      if (e1 > s1)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s1), "r"((uint32_t)(e1 - s1)) : "memory");
+    }
+  };
+  zero_cnt(cnt_bytes);
+  if (tid == 0) { s_ncol = 0; s_nbig = 0; s_np = 0; s_n3 = 0; }
+  __syncthreads();
+  unsigned long long done = 0;
+  Rec<R> r[IL];
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = clock64(), tB = 0;
+#define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
+#else
+#define RS_PROF(i) do { } while (0)
+#endif
+  auto next_bin = [&](uint32_t b) {  // bins <= C are k_local's
+    while (b < nlist && list[b].len <= C) b += ncl;
+    return b;
+  };
+  auto load = [&](const Seg& g) {  // this CTA's part of bin g into registers
+    const uint32_t pt = (g.len + CS - 1) / CS, q0 = min(g.len, crank * pt), qn = min(g.len, q0 + pt) - q0;
+    const uint8_t* src = buf_of(g.src, recs, tmp) + ((size_t)g.off + q0 + tid) * R;
+#pragma unroll
+    for (int i = 0; i < IL; ++i)
+      if ((uint32_t)(i * LB + tid) < qn) r[i] = ldg_rec<R>(src + (size_t)i * LB * R);
+  };
+  uint32_t bi = next_bin(blockIdx.x / CS);
+  Seg sg;
+  if (bi < nlist) {
+    sg = list[bi];
+    load(sg);
+    prefetch_l2(next_bin(bi + ncl));
+  }
+  bool pending = false;  // a bulk store still reads the stage
+  while (bi < nlist) {
+    const uint32_t n = sg.len, d = sg.depth;
+    const uint32_t part = (n + CS - 1) / CS, p0 = min(n, crank * part), pn = min(n, p0 + part) - p0;
+    const uint32_t W = max(local_width(n, wmax), WMIN);
+    const uint32_t Wl = W - LCS, slice = 1u << Wl;
+    // 1. private ranks
+    constexpr int IP = (IL + 1) / 2;
+    uint32_t rk[IP];
+#pragma unroll
+    for (int i = 0; i < IP; ++i) rk[i] = 0;
+#pragma unroll
+    for (int i = 0; i < IL; ++i) {
+      if ((uint32_t)(i * LB + tid) < pn) {
+        const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W), sh = 16u * (b & 1u);
+        const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
+        rk[i >> 1] |= old << (16 * (i & 1));
+      }
+    }
+    cl.sync();  // every CTA has counted
+    RS_PROF(0);
+    // 2. slice owner: totals, starts, collision list, per-CTA bases
+    const uint32_t nch = slice / 8u, m = nch / LB, c0 = (uint32_t)tid * m;
+    uint4* sst4 = reinterpret_cast<uint4*>(sst);
+    uint32_t T = 0, np = 0;
+    bool cst = false;
+    auto eqn = [&](uint32_t x) { return (x & 0xffffu) == n || (x >> 16) == n; };
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t ch = crank * nch + c0 + j;
+      uint4 t = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < CS; ++k) {
+        const uint4 v = reinterpret_cast<const uint4*>(cl.map_shared_rank(cnt, (uint32_t)k))[ch];
+        t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      }
+      sst4[c0 + j] = t;
+      const uint32_t p = t.x + t.y + t.z + t.w;
+      T += (p & 0xffffu) + (p >> 16);
+      cst |= eqn(t.x) | eqn(t.y) | eqn(t.z) | eqn(t.w);
+      const uint32_t tw[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) np += ((tw[q >> 1] >> (16 * (q & 1))) & 0xffffu) == 2u;
+    }
+    np = __reduce_add_sync(0xffffffffu, np);  // pairs: listed first, so that the fix-up warps stay uniform
+    if (lane == 0 && np) atomicAdd(&s_np, np);
+    cst = __syncthreads_or(cst);
+    uint32_t inc = T;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t tot = 0, carry = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      carry += w < warp ? wsum[w] : 0u;
+      tot += wsum[w];
+    }
+    uint32_t s = carry + inc - T;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t ch = crank * nch + c0 + j;
+      const uint4 t = sst4[c0 + j];
+      uint4 o4;
+      o4.x = s * 0x10001u + (t.x << 16); s += (t.x & 0xffffu) + (t.x >> 16);
+      o4.y = s * 0x10001u + (t.y << 16); s += (t.y & 0xffffu) + (t.y >> 16);
+      o4.z = s * 0x10001u + (t.z << 16); s += (t.z & 0xffffu) + (t.z >> 16);
+      o4.w = s * 0x10001u + (t.w << 16); s += (t.w & 0xffffu) + (t.w >> 16);
+      sst4[c0 + j] = o4;
+      uint4 v[CS];
+#pragma unroll
+      for (int k = 0; k < CS; ++k) v[k] = reinterpret_cast<const uint4*>(cl.map_shared_rank(cnt, (uint32_t)k))[ch];
+      // buckets of >= 2 records join the collision list (one list append per warp)
+      const uint32_t tw[4] = {t.x, t.y, t.z, t.w};
+      uint32_t cm2 = 0, cm3 = 0;  // buckets of 2, and of >= 3 records
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t c = (tw[q >> 1] >> (16 * (q & 1))) & 0xffffu;
+        cm2 |= (uint32_t)(c == 2u) << q;
+        cm3 |= (uint32_t)(c >= 3u) << q;
+      }
+      const uint32_t cc = __popc(cm2) | __popc(cm3) << 16;  // both counts, one scan
+      uint32_t ci = cc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, ci, o);
+        if (lane >= o) ci += y;
+      }
+      uint32_t b2 = 0, b3 = 0;
+      if (lane == 31) {
+        if (ci & 0xffffu) b2 = atomicAdd(&s_ncol, ci & 0xffffu);
+        if (ci >> 16) b3 = s_np + atomicAdd(&s_n3, ci >> 16);
+      }
+      const uint32_t ex = ci - cc;
+      b2 = __shfl_sync(0xffffffffu, b2, 31) + (ex & 0xffffu);
+      b3 = __shfl_sync(0xffffffffu, b3, 31) + (ex >> 16);
+      while (cm2) {
+        const int q = __ffs(cm2) - 1;
+        cm2 &= cm2 - 1u;
+        blist[b2++] = (c0 + j) * 8u + (uint32_t)q;
+      }
+      while (cm3) {
+        const int q = __ffs(cm3) - 1;
+        cm3 &= cm3 - 1u;
+        blist[b3++] = (c0 + j) * 8u + (uint32_t)q;
+      }
+      uint4 run = o4;  // CTA k's records of a bucket follow those of CTAs < k
+#pragma unroll
+      for (int k = 0; k < CS; ++k) {
+        reinterpret_cast<uint4*>(cl.map_shared_rank(cnt, (uint32_t)k))[ch] = run;
+        run.x += v[k].x; run.y += v[k].y; run.z += v[k].z; run.w += v[k].w;
+      }
+    }
+    if (tid < CS) cl.map_shared_rank(s_tot, (uint32_t)tid)[crank] = cst ? 0xffffffffu : tot;
+    if (pending && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    pending = false;
+    cl.sync();  // bases and slice totals in place; the stage is free
+    RS_PROF(1);
+    uint32_t off[CS], mine = 0;
+    {
+      uint32_t run = 0;
+      bool over = false;
+#pragma unroll
+      for (int o = 0; o < CS; ++o) {
+        off[o] = run;
+        run += s_tot[o];
+        over |= s_tot[o] > stage_cap;
+      }
+      mine = s_tot[crank];
+      if (over) {  // skewed slices or a constant composite digit: the next level's Large list takes the bin
+        if (crank == 0 && tid == 0) {
+          Seg ns = sg;
+          ns.mode = MODE_NONE;
+          large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+        }
+        __syncthreads();
+        zero_cnt(2u << W);
+        if (tid == 0) { s_ncol = 0; s_nbig = 0; s_np = 0; s_n3 = 0; }
+        __syncthreads();
+        bi = next_bin(bi + ncl);
+        if (bi < nlist) {
+          sg = list[bi];
+          load(sg);
+          prefetch_l2(next_bin(bi + ncl));
+        }
+        continue;
+      }
+    }
+    // 3. one remote store per record
+#pragma unroll
+    for (int i = 0; i < IL; ++i) {
+      if ((uint32_t)(i * LB + tid) < pn) {
+        const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+        const uint32_t pos = (uint32_t)cnt16[b] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+        const uint32_t o = b >> Wl;
+        st_rec<R>((o == crank ? stage : cl.map_shared_rank(stage, o)) + (size_t)pos * R, r[i]);
+      }
+    }
+    // staged (this CTA's slice complete): split cluster barrier; the next
+    // bin's records load between arrive and wait and while this one is finished
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    const uint32_t nb = next_bin(bi + ncl);
+    Seg nsg;
+    if (nb < nlist) {
+      nsg = list[nb];
+      load(nsg);
+      prefetch_l2(next_bin(nb + ncl));
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    RS_PROF(2);
+    // 4. finish the slice
+    const bool fix = 8 * ((int)K - (int)d) > (int)W;
+    uint8_t* out = recs + ((size_t)sg.off + off[crank]) * R;
+    const bool bulk = mine && (((uintptr_t)out | ((uintptr_t)mine * R)) & 15u) == 0;
+    local_finish<R, K, LB, NTW>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice, d, W,
+                                fix ? s_np + s_n3 : 0u, &s_nbig, reinterpret_cast<TailScratch<K>*>(cnt), out,
+                                sg.off + off[crank], local_next, nxt, ctl, bulk
+#ifdef RADSORT_PHASE_PROF
+                                , pf + 4
+#endif
+    );
+    pending = bulk;
+    done += mine;
+    __syncthreads();
+    RS_PROF(3);
+    zero_cnt(2u << W);
+    if (tid == 0) { s_ncol = 0; s_nbig = 0; s_np = 0; s_n3 = 0; }
+    __syncthreads();
+    bi = nb;
+    sg = nsg;
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid == 0 && done) atomicAdd(&ctl->rec_local, done);
+#ifdef RADSORT_PHASE_PROF
+  if (tid == 0) {
+    for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[8 + q], pf[q]);
+  }
+#endif
+#undef RS_PROF
+  cl.sync();  // no CTA leaves while peers may still access its shared memory
 }
 
 // -------------------------------------------------------------- k_bounds

@@ -37,6 +37,67 @@ struct Sorter {
                                                ctl, recs, tmp);
   }
 
+  // ---- cluster-local sort (bins of C < n <= CCAP records, k_local_cluster)
+  static constexpr int CS = 4;
+  static constexpr uint32_t LCS = 2;
+  static constexpr uint32_t CL_W = R >= 24 ? 14 : 15;                     // composite digit width cap
+  static constexpr size_t CL_CNT = (size_t)2 << CL_W;                      // 2^W u16 counters / bases
+  static constexpr size_t CL_SST = CL_CNT >> LCS;                          // the slice's bucket starts
+  static constexpr uint32_t CL_STAGE_CAP = (uint32_t)((LOCAL_SMEM_MAX - CL_CNT - CL_SST - 2048) / (R + 2));
+  static constexpr int CL_ILMAX = R <= 8 ? 32 : (R <= 16 ? 16 : 8);  // register budget of the record array
+  static constexpr uint32_t CCAP_SMEM = CL_STAGE_CAP / 5 * 4 * CS;       // 20 % slack for uneven bucket slices
+  static constexpr uint32_t CCAP = CCAP_SMEM < (uint32_t)(CL_ILMAX * 512 * CS) ? CCAP_SMEM : CL_ILMAX * 512 * CS;
+
+  template <int IL>
+  static void launch_cluster_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
+                               Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+    const uint32_t wmax = CL_W;
+    const size_t stage_bytes = ((size_t)CL_STAGE_CAP * R + 15) & ~(size_t)15;
+    const uint32_t cap = CL_STAGE_CAP / 2 + 1;
+    const size_t smem = stage_bytes + CL_CNT + CL_SST + (((size_t)cap * 4 + 15) & ~(size_t)15);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_local_cluster<R, K, IL, 512, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)LOCAL_SMEM_MAX);
+      attr = true;
+    }
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CS * sms / CS, 1, 1);
+      cfg.blockDim = dim3(512, 1, 1);
+      cfg.dynamicSmemBytes = LOCAL_SMEM_MAX;
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, k_local_cluster<R, K, IL, 512, CS>, &cfg) != cudaSuccess ||
+          max_clusters <= 0) {
+        cudaGetLastError();
+        max_clusters = sms / CS;
+      }
+    }
+    const unsigned clusters = (unsigned)std::max<size_t>(1, std::min<size_t>(nloc, (size_t)max_clusters));
+    k_local_cluster<R, K, IL, 512, CS><<<clusters * CS, 512, smem, st>>>(
+        list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)CL_CNT, cap, next, nxt, large_next, ctl, recs, tmp);
+  }
+
+  static void launch_cluster(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
+                             Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+    const uint32_t il = (maxlen + CS * 512 - 1) / (CS * 512);  // records per thread
+#define RS_CL(IL) launch_cluster_t<IL>(nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st, sms)
+    if (il <= 2) RS_CL(2);
+    else if (il <= 4) RS_CL(4);
+    else if constexpr (R <= 32) {
+      if (il <= 8) RS_CL(8);
+      else if constexpr (R <= 8) {
+        if (il <= 16) RS_CL(16);
+        else RS_CL(32);
+      } else if constexpr (R <= 16) {
+        RS_CL(16);
+      }
+    } else {
+      RS_CL(8);
+    }
+#undef RS_CL
+  }
+
   static void set_attrs() {
     static bool done = false;
     if (done) return;
@@ -47,8 +108,14 @@ struct Sorter {
   // Local bins of up to `maxlen` records: IL records per thread, at most 256
   // bytes of records per thread; 256-thread CTAs (two per SM) unless the bins
   // need 512 threads.
-  static void launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
-                           uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+  // Returns true when a cluster launch may have handed bins to the next level's Large list.
+  static bool launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
+                           Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+    if (maxlen > C) {  // the list holds cluster-size bins: k_local takes the rest at full capacity
+      launch_local_t<(int)((C + 511) / 512), 512>(nloc, C, list, next, nxt, ctl, recs, tmp, st, sms);
+      launch_cluster(nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st, sms);
+      return true;
+    }
     // small bins (up to 256 B of records per thread at 64 threads): 64-thread
     // CTAs, so that many bins are in flight per SM (the per-bin phases are
     // latency-bound)
@@ -63,12 +130,12 @@ struct Sorter {
         else if constexpr (ILS >= 16) RS_LOCAL_S(16);
       }
 #undef RS_LOCAL_S
-      return;
+      return false;
     }
     constexpr int ILMAX = (int)((C + 511) / 512);  // records per thread at 512 threads
     if ((size_t)maxlen > (size_t)256 * ILMAX) {
       launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms);
-      return;
+      return false;
     }
     const uint32_t il = (maxlen + 255) / 256;
 #define RS_LOCAL(IL) launch_local_t<IL, 256>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms)
@@ -81,6 +148,7 @@ struct Sorter {
     else if (il <= 16) RS_LOCAL(16);
     else RS_LOCAL(ILMAX);
 #undef RS_LOCAL
+    return false;
   }
 
   struct Views {
@@ -179,6 +247,11 @@ struct Sorter {
     Ctl* ctl = v.ctl;
     const size_t tiles_max = v.tiles_max;
 
+    // cluster-local sorting of bins above C: on for R >= 24 (where C is small
+    // and it replaces a full radix level; measured); RADSORT_CLUSTER=1
+    // forces it on, =0 off
+    const char* cl_env = getenv("RADSORT_CLUSTER");
+    const bool cluster_ok = cl_env ? cl_env[0] == '1' : R >= 24;
     int occ_s = 0, occ_h = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB, false>, SB, TB);
     const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
@@ -285,7 +358,7 @@ struct Sorter {
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
-                                                                  tmp, v.probes);
+                                                                  tmp, v.probes, cluster_ok ? CCAP : C);
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
         stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry
@@ -299,7 +372,7 @@ struct Sorter {
       RS_CUDA(cudaGetLastError());
       RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       RS_CUDA(cudaStreamSynchronize(st));
-      const Ctl c = *ctx->h_ctl;
+      Ctl c = *ctx->h_ctl;
       if (level == 0) stats.first_digit = c.d0;
       const uint32_t nloc = c.n_local[cur];
       if (log)
@@ -307,10 +380,16 @@ struct Sorter {
                 c.tiles_total, c.n_large_next, nloc, c.max_local_len[cur]);
       if (nloc) {
         tm.begin(RADSORT_K_LOCAL);
-        launch_local(nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, ctl, recs, tmp, st, ctx->sms);
+        const bool cl = launch_local(nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, L[nxt], ctl, recs, tmp, st,
+                                     ctx->sms);
         tm.end();
-        stats.kernel_launches[RADSORT_K_LOCAL]++;
+        stats.kernel_launches[RADSORT_K_LOCAL] += cl ? 2 : 1;
         RS_CUDA(cudaGetLastError());
+        if (cl) {  // the cluster sort may have handed bins back as Large bins of the next level
+          RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+          RS_CUDA(cudaStreamSynchronize(st));
+          c.n_large_next = ctx->h_ctl->n_large_next;
+        }
       }
       stats.levels = level + 1;
       if (log && tm.on) {  // per-level kernel times (radsort_set_timing(1) + RADSORT_LOG=1)

@@ -237,3 +237,55 @@ def test_kmer_device_generator_matches_host():
         h = dg.generate(5000, R, K, "kmer", seed=3, first=77)
         d = dd.generate_tensor(5000, R, K, "kmer", seed=3, first=77).cpu().numpy()
         assert np.array_equal(h, d)
+
+
+def _top_word(a: np.ndarray, K: int):
+    w = a.view(np.uint64).reshape(a.shape[0], -1)
+    return w, K // 8 - 1  # the most significant key word
+
+
+@pytest.fixture
+def force_cluster(monkeypatch):
+    # the cluster local sort is on by default for R >= 24 only; force it for every layout
+    monkeypatch.setenv("RADSORT_CLUSTER", "1")
+
+
+@pytest.mark.parametrize("R,K", LAYOUTS)
+def test_cluster_local_bins(R, K, force_cluster):
+    # level-0 bins of ~2.5 C records (C < len <= the cluster capacity): sorted
+    # by the 4-CTA cluster local sort (k_local_cluster), with a ragged tail
+    import paper_1703_00687_b200 as rs
+
+    n = 256 * (C_of(R) * 5 // 2) + 77
+    check(dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=R * 3 + K), K)
+    assert rs.last_stats()["scatter_passes"] == 1  # every level-0 bin was sorted on chip
+
+
+@pytest.mark.parametrize("R,K", [(16, 8), (32, 16)])
+def test_cluster_off_matches(R, K, monkeypatch):
+    monkeypatch.setenv("RADSORT_CLUSTER", "0")
+    n = 256 * (C_of(R) * 5 // 2) + 77
+    check(dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=R * 5 + K), K)
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 16), (32, 16)])
+@pytest.mark.parametrize("mode", ["one_slice", "constant", "split_slices"])
+def test_cluster_local_bins_handed_back(R, K, mode, force_cluster):
+    # the same bin sizes with a skewed digit 1: "one_slice" (digit 1 < 16: every
+    # record of a bin lands in one CTA's bucket slice) and "constant" (digits
+    # 1-2 constant: the composite digit is constant) make the cluster sort hand
+    # the bins back to the next level's Large list; "split_slices" (half the
+    # records share digits 1-2 = 0x92 0x34, the rest digit 1 < 16) fits, leaving
+    # one huge colliding bucket for the next Local level.  Exact in all cases.
+    n = 256 * (C_of(R) * 5 // 2) + 5
+    a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=11)
+    w, t = _top_word(a, K)
+    keep_top = np.uint64(0xFF00_00FF_FFFF_FFFF)
+    if mode == "one_slice":
+        w[:, t] &= np.uint64(0xFF0F_FFFF_FFFF_FFFF)
+    elif mode == "constant":
+        w[:, t] = (w[:, t] & keep_top) | np.uint64(0x0012_3400_0000_0000)
+    else:
+        w[::2, t] &= np.uint64(0xFF0F_FFFF_FFFF_FFFF)
+        w[1::2, t] = (w[1::2, t] & keep_top) | np.uint64(0x0092_3400_0000_0000)
+    check(a, K)
