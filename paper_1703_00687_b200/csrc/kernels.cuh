@@ -423,7 +423,23 @@ template <int K>
 struct TailScratch {
   uint32_t cnt[RADIX];      // digit counters, then packed (start << 16 | count)
   Key<K> key[TINY_MAX];     // keys in partitioned order
+  uint32_t ltm[TINY_MAX / 32], eqm[TINY_MAX / 32];  // per slot: key < / == its sub-bin's pivot
 };
+
+// number of set bits of the TINY_MAX-bit mask m in [a, b)
+__device__ __forceinline__ uint32_t popc_range(const uint32_t* m, uint32_t a, uint32_t b) {
+  uint32_t s = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < TINY_MAX / 32; ++w) {
+    const uint32_t x0 = max(a, w * 32u), x1 = min(b, w * 32u + 32u);
+    if (x0 < x1) {
+      const uint32_t len = x1 - x0;
+      const uint32_t mk = (len == 32u ? 0xffffffffu : ((1u << len) - 1u)) << (x0 - w * 32u);
+      s += __popc(m[w] & mk);
+    }
+  }
+  return s;
+}
 
 // Tail sorter for a bin of 2 <= n <= TINY_MAX records, one warp (PAPER.md
 // §3.3, GPU form).  One counting pass on digit `depth` with warp-private smem
@@ -494,14 +510,65 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
     }
     __syncwarp();
   }
+  // mixed sub-bins of > HV records (typically many copies of one key and a
+  // few others): three-way classification against a pivot key (the sub-bin's
+  // middle slot), so that ES runs only among the records below / above it and
+  // the pivot's copies are placed by slot order -- O(c * m) instead of O(c^2)
+  // for m records different from the pivot
+  constexpr uint32_t HV = 8;
+  uint32_t mx = 0;  // bit e: record e sits in a mixed sub-bin
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t i = (uint32_t)(e * 32 + lane);
+    if (i < n && (pr[e] >> 16) > 1u && (!checked || (ws.cnt[digit_of(k[e], depth)] & 0x8000u) != 0u)) mx |= 1u << e;
+  }
+  bool heavy = false;
+#pragma unroll
+  for (int e = 0; e < E; ++e) heavy |= ((mx >> e) & 1u) && (pr[e] >> 16) > HV;
+  heavy = __any_sync(0xffffffffu, heavy);
+  if (heavy) {
+    if (lane < (int)(TINY_MAX / 32)) { ws.ltm[lane] = 0; ws.eqm[lane] = 0; }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
+      if (((mx >> e) & 1u) && c > HV) {
+        const Key<K> pv = ws.key[s0 + c / 2];
+        if (key_lt(k[e], pv)) atomicOr(&ws.ltm[slot >> 5], 1u << (slot & 31u));
+        else if (key_eq(k[e], pv)) atomicOr(&ws.eqm[slot >> 5], 1u << (slot & 31u));
+      }
+    }
+    __syncwarp();
+  }
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const uint32_t i = (uint32_t)(e * 32 + lane);
     if (i < n) {
       const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
       uint32_t fin = slot;
-      const bool mixed = !checked || (ws.cnt[digit_of(k[e], depth)] & 0x8000u) != 0u;
-      if (c > 1 && mixed) {  // ES among the sub-bin's c records (pairs / triples: predicated, no divergent loop)
+      const bool mixed = (mx >> e) & 1u;
+      if (mixed && c > HV) {
+        const uint32_t bit = 1u << (slot & 31u);
+        const uint32_t nlt = popc_range(ws.ltm, s0, s0 + c);
+        if (ws.eqm[slot >> 5] & bit) {
+          fin = s0 + nlt + popc_range(ws.eqm, s0, slot);
+        } else {  // ES among the records on the same side of the pivot
+          const bool lt = (ws.ltm[slot >> 5] & bit) != 0u;
+          uint32_t r = lt ? 0u : nlt + popc_range(ws.eqm, s0, s0 + c);
+          for (uint32_t w = s0 >> 5; w <= (s0 + c - 1u) >> 5; ++w) {
+            uint32_t m = lt ? ws.ltm[w] : ~(ws.ltm[w] | ws.eqm[w]);
+            const uint32_t lo = max(s0, w * 32u) - w * 32u, hi = min(s0 + c, w * 32u + 32u) - w * 32u;
+            m &= (hi - lo == 32u ? 0xffffffffu : ((1u << (hi - lo)) - 1u) << lo);
+            while (m) {
+              const uint32_t q = w * 32u + (uint32_t)(__ffs(m) - 1);
+              m &= m - 1u;
+              const Key<K> kq = ws.key[q];
+              r += (uint32_t)key_lt(kq, k[e]) | ((uint32_t)(q < slot) & (uint32_t)key_eq(kq, k[e]));
+            }
+          }
+          fin = s0 + r;
+        }
+      } else if (c > 1 && mixed) {  // ES among the sub-bin's c records (pairs / triples: predicated, no divergent loop)
         uint32_t r = 0;
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {

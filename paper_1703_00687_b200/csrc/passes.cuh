@@ -1021,6 +1021,9 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
       atomicMax(&ctl->max_local_len[nxt], c);
     }
   }
+#ifdef RADSORT_PHASE_PROF
+  if (pfx && tid == 0) pfx[3] += clock64() - fA;
+#endif
   return true;
 }
 
@@ -1078,6 +1081,9 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #define RS_PROF(i) do { } while (0)
 #endif
   constexpr int IP = (IL + 1) / 2;  // ranks < 2^16: two per register
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long pfl[4] = {0, 0, 0, 0};
+#endif
   for (;;) {
     const uint32_t n = sg.len;
     const int lim = (int)n - tid;
@@ -1190,7 +1196,11 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
       __syncthreads();  // staged
       RS_PROF(3);
       tail = local_finish<R, K, LB, NW>(stage, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
-                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl);
+                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl
+#ifdef RADSORT_PHASE_PROF
+                                       , false, pfl
+#endif
+      );
     }
     done += n;
     __syncthreads();
@@ -1205,6 +1215,10 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #ifdef RADSORT_PHASE_PROF
   if (tid == 0) {
     for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[8 + q], pf[q]);
+    atomicAdd(&ctl->prof[0], pfl[0]);
+    atomicAdd(&ctl->prof[6], pfl[1]);
+    atomicAdd(&ctl->prof[7], pfl[2]);
+    atomicAdd(&ctl->prof[12], pfl[3]);
   }
 #endif
 #undef RS_PROF

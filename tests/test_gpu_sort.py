@@ -289,3 +289,23 @@ def test_cluster_local_bins_handed_back(R, K, mode, force_cluster):
         w[::2, t] &= np.uint64(0xFF0F_FFFF_FFFF_FFFF)
         w[1::2, t] = (w[1::2, t] & keep_top) | np.uint64(0x0092_3400_0000_0000)
     check(a, K)
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 16), (32, 16), (24, 8)])
+@pytest.mark.parametrize("per_bin", [20, 100, 128])
+def test_tail_sorter_dominant_key_pivot(R, K, per_bin):
+    # tiny bins (<= 128 records, the warp tail sorter) made of many copies of
+    # one key plus a few keys that differ only in the last byte, above and
+    # below it: the pivot three-way path of the tail sorter's ES
+    n = 256 * per_bin
+    a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=per_bin + R)
+    w, t = _top_word(a, K)
+    top = w[:, t] & np.uint64(0xFF00_0000_0000_0000)
+    w[:, t] = top | np.uint64(0x0012_3456_789A_BC80)
+    if K == 16:
+        w[:, 0] = np.uint64(0x1111_2222_3333_4480)
+    rng = np.random.default_rng(per_bin)
+    odd = rng.random(n) < 0.08
+    low = rng.integers(0, 256, n).astype(np.uint64)
+    w[odd, 0] = (w[odd, 0] & ~np.uint64(0xFF)) | low[odd]
+    check(a, K)
