@@ -448,7 +448,7 @@ __device__ __forceinline__ uint32_t popc_range(const uint32_t* m, uint32_t a, ui
 // place by enumeration sort among those c records only (PAPER.md:102-104 ES:
 // n comparisons, one move per record; ties by partition slot).  Works on keys;
 // each full record is then moved once, src -> out.  src and out must not alias.
-template <int R, int K, int E>
+template <int R, int K, int E, bool PV>
 __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
                                                  TailScratch<K>& ws) {
   uint4* w4 = reinterpret_cast<uint4*>(ws.cnt);
@@ -515,24 +515,22 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
   // middle slot), so that ES runs only among the records below / above it and
   // the pivot's copies are placed by slot order -- O(c * m) instead of O(c^2)
   // for m records different from the pivot
-  constexpr uint32_t HV = 8;
-  uint32_t mx = 0;  // bit e: record e sits in a mixed sub-bin
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const uint32_t i = (uint32_t)(e * 32 + lane);
-    if (i < n && (pr[e] >> 16) > 1u && (!checked || (ws.cnt[digit_of(k[e], depth)] & 0x8000u) != 0u)) mx |= 1u << e;
-  }
+  constexpr uint32_t HV = PV ? 8u : 0xffffu;  // PV = false: no pivot path (callers short of registers)
+  auto is_mixed = [&](int e) {
+    return (uint32_t)(e * 32 + lane) < n && (pr[e] >> 16) > 1u &&
+           (!checked || (ws.cnt[digit_of(k[e], depth)] & 0x8000u) != 0u);
+  };
   bool heavy = false;
 #pragma unroll
-  for (int e = 0; e < E; ++e) heavy |= ((mx >> e) & 1u) && (pr[e] >> 16) > HV;
-  heavy = __any_sync(0xffffffffu, heavy);
+  for (int e = 0; e < E; ++e) heavy |= (uint32_t)(e * 32 + lane) < n && (pr[e] >> 16) > HV;
+  heavy = PV && __any_sync(0xffffffffu, heavy);
   if (heavy) {
     if (lane < (int)(TINY_MAX / 32)) { ws.ltm[lane] = 0; ws.eqm[lane] = 0; }
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
-      if (((mx >> e) & 1u) && c > HV) {
+      if (c > HV && is_mixed(e)) {
         const Key<K> pv = ws.key[s0 + c / 2];
         if (key_lt(k[e], pv)) atomicOr(&ws.ltm[slot >> 5], 1u << (slot & 31u));
         else if (key_eq(k[e], pv)) atomicOr(&ws.eqm[slot >> 5], 1u << (slot & 31u));
@@ -546,8 +544,8 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
     if (i < n) {
       const uint32_t slot = pr[e] & 0xffu, s0 = (pr[e] >> 8) & 0xffu, c = pr[e] >> 16;
       uint32_t fin = slot;
-      const bool mixed = (mx >> e) & 1u;
-      if (mixed && c > HV) {
+      const bool mixed = !checked || (ws.cnt[digit_of(k[e], depth)] & 0x8000u) != 0u;
+      if (heavy && c > HV && mixed) {
         const uint32_t bit = 1u << (slot & 31u);
         const uint32_t nlt = popc_range(ws.ltm, s0, s0 + c);
         if (ws.eqm[slot >> 5] & bit) {
@@ -587,12 +585,12 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
   __syncwarp();
 }
 
-template <int R, int K>
+template <int R, int K, bool PV = true>
 __device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
                                                TailScratch<K>& ws) {
-  if (n <= 32) warp_tail_sort_e<R, K, 1>(src, out, n, depth, lane, ws);
-  else if (n <= 64) warp_tail_sort_e<R, K, 2>(src, out, n, depth, lane, ws);
-  else warp_tail_sort_e<R, K, 4>(src, out, n, depth, lane, ws);
+  if (n <= 32) warp_tail_sort_e<R, K, 1, PV>(src, out, n, depth, lane, ws);
+  else if (n <= 64) warp_tail_sort_e<R, K, 2, PV>(src, out, n, depth, lane, ws);
+  else warp_tail_sort_e<R, K, 4, PV>(src, out, n, depth, lane, ws);
 }
 
 }  // namespace radsort

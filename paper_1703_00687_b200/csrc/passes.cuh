@@ -943,7 +943,7 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* 
 // Steps 4-6 of the CTA-local sort, for a bin staged in smem in bucket order
 // (see k_local).  All threads of the CTA call it (it contains barriers).
 // Returns true when the tail sorter used the counter region as scratch.
-template <int R, int K, int LB, int NTW>
+template <int R, int K, int LB, int NTW, bool PV = true>
 __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* start16, uint32_t* blist, uint32_t cap,
                                              uint32_t n, uint32_t nbk, uint32_t d, uint32_t W, uint32_t ncol,
                                              uint32_t* s_nbig, TailScratch<K>* tsc, uint8_t* out, uint32_t off,
@@ -1014,7 +1014,7 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
     if (!(en >> 31)) continue;
     const uint32_t s0 = en & 0xffffu, c = (en >> 16) & 0x7fffu;
     if (c <= TINY_MAX) {
-      warp_tail_sort<R, K>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc[warp]);
+      warp_tail_sort<R, K, PV>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc[warp]);
     } else if (lane == 0) {
       Seg ns = {off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
       local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
@@ -1195,7 +1195,9 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
       RS_PROF(2);
       __syncthreads();  // staged
       RS_PROF(3);
-      tail = local_finish<R, K, LB, NW>(stage, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
+      // the tail sorter's pivot path only in the small-bin configuration (duplicate-heavy
+      // streams of small bins live there; the big-bin ones are short of registers)
+      tail = local_finish<R, K, LB, NW, LB == 64>(stage, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
                                        reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl
 #ifdef RADSORT_PHASE_PROF
                                        , false, pfl
@@ -1487,7 +1489,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     const bool fix = 8 * ((int)K - (int)d) > (int)W;
     uint8_t* out = recs + ((size_t)sg.off + off[crank]) * R;
     const bool bulk = mine && (((uintptr_t)out | ((uintptr_t)mine * R)) & 15u) == 0;
-    local_finish<R, K, LB, NTW>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice, d, W,
+    local_finish<R, K, LB, NTW, false>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice, d, W,
                                 fix ? s_np + s_n3 : 0u, &s_nbig, reinterpret_cast<TailScratch<K>*>(cnt), out,
                                 sg.off + off[crank], local_next, nxt, ctl, bulk
 #ifdef RADSORT_PHASE_PROF

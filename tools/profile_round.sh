@@ -15,14 +15,17 @@ done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2> $O/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/c2_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
-for c in c2 c5; do
+for c in ${FULL-c2 c5}; do  # FULL="" skips (the return limit is 64 MiB)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_local|k_hist_pre" -c 5 \
     -o $O/${c}_full python bench.py --config $c --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_$c.log 2>&1
 done
+# the cluster local sort (c4's dominant phase): one full capture
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_local_cluster" -c 1 \
+  -o $O/c4_cluster_full python bench.py --config c4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_c4cl.log 2>&1
 # DRAM bytes per launch only (small reports; the gpurun return limit is 64 MiB)
-for c in c3 c4; do
+for c in c3 c4 kmc; do
   timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    -k regex:"k_scatter|k_local|k_hist_pre" -c 8 \
+    -k regex:"k_scatter|k_local|k_hist_pre|k_children" -c 12 \
     -o $O/${c}_dram python bench.py --config $c --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_$c.log 2>&1
 done
 ls -la $O
