@@ -602,11 +602,13 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
                      (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
         }
       }
-      uint32_t rk[I];
+      uint32_t rk[(I + 1) / 2];  // ranks < T <= 2^16: two per register (fewer live registers under the cap)
+#pragma unroll
+      for (int i = 0; i < (I + 1) / 2; ++i) rk[i] = 0;
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
-        if (idx < m) rk[i] = atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u);
+        if (idx < m) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u) << (16 * (i & 1));
       }
       __syncthreads();
       RS_PROF(1);
@@ -624,7 +626,9 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
-        if (idx < m) st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + rk[i]) * R, r[i]);
+        if (idx < m)
+          st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)) * R,
+                    r[i]);
       }
       __syncthreads();  // r[] free, sh_t/sh_s hold the next ticket
       const uint32_t tn = sh_t, sn = sh_s;
