@@ -529,6 +529,8 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
 // digit, obtain each digit's global offset by single-pass decoupled look-back
 // over the segment's tiles, and write every digit run with coalesced stores.
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
+constexpr int SCATTER_PAD = 64;  // dynamic smem beyond the TB-byte tile: the pad slot of absent records
+
 template <int R, int K, int TB, int SB, int MINB, bool PRE>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
-  __shared__ uint32_t cnt[RADIX], start[RADIX], gofs[RADIX], ws[8];
+  __shared__ uint32_t cnt[RADIX + 1], start[RADIX], gofs[RADIX], ws[8];  // cnt[RADIX]: absent records
   __shared__ uint32_t sh_t, sh_s;
   const int tid = threadIdx.x;
   const uint32_t total = ctl->tiles_total;
@@ -605,10 +607,13 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       uint32_t rk[(I + 1) / 2];  // ranks < T <= 2^16: two per register (fewer live registers under the cap)
 #pragma unroll
       for (int i = 0; i < (I + 1) / 2; ++i) rk[i] = 0;
+      // branch-free: an absent record (ragged last tile) counts in cnt[RADIX]
+      // and is staged in the pad slot T (no divergent branches around the atomics)
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
-        if (idx < m) rk[i >> 1] |= atomicAdd(&cnt[digit_of(key_of<R, K>(r[i]), d)], 1u) << (16 * (i & 1));
+        const uint32_t dg = idx < m ? digit_of(key_of<R, K>(r[i]), d) : (uint32_t)RADIX;
+        rk[i >> 1] |= atomicAdd(&cnt[dg], 1u) << (16 * (i & 1));
       }
       __syncthreads();
       RS_PROF(1);
@@ -626,9 +631,8 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
-        if (idx < m)
-          st_rec<R>(stage + (size_t)(start[digit_of(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu)) * R,
-                    r[i]);
+        const uint32_t pos = start[digit_of(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+        st_rec<R>(stage + (size_t)(idx < m ? pos : T) * R, r[i]);
       }
       __syncthreads();  // r[] free, sh_t/sh_s hold the next ticket
       const uint32_t tn = sh_t, sn = sh_s;

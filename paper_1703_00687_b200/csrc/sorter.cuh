@@ -230,8 +230,8 @@ struct Sorter {
     set_attrs();
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
-      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
+      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB + SCATTER_PAD);
+      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB + SCATTER_PAD);
       attr = true;
     }
     Views v;
@@ -253,7 +253,7 @@ struct Sorter {
     const char* cl_env = getenv("RADSORT_CLUSTER");
     const bool cluster_ok = cl_env ? cl_env[0] == '1' : R >= 24;
     int occ_s = 0, occ_h = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB, false>, SB, TB);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB, false>, SB, TB + SCATTER_PAD);
     const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
     const char* hg = getenv("RADSORT_HIST_CTAS_PER_SM");
     const unsigned hist_grid = (unsigned)ctx->sms * (hg ? atoi(hg) : 4);  // chunks of the reduce-then-scan prefix
@@ -348,11 +348,11 @@ struct Sorter {
         const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
         tm.begin(RADSORT_K_SCATTER);
         if (pre)
-          k_scatter<R, K, TB, SB, MINB, true><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
+          k_scatter<R, K, TB, SB, MINB, true><<<gs, SB, TB + SCATTER_PAD, st>>>(L[cur], tile_start, n_large, segbase, status,
                                                                   ctx->epoch, ctl, recs, tmp, tile_pre, ch_first,
                                                                   carry_in, hist_grid, v.splitc, v.probes, v.tile_seg);
         else
-          k_scatter<R, K, TB, SB, MINB, false><<<gs, SB, TB, st>>>(L[cur], tile_start, n_large, segbase, status,
+          k_scatter<R, K, TB, SB, MINB, false><<<gs, SB, TB + SCATTER_PAD, st>>>(L[cur], tile_start, n_large, segbase, status,
                                                                    ctx->epoch, ctl, recs, tmp, nullptr, nullptr,
                                                                    nullptr, 0, v.splitc, v.probes, v.tile_seg);
         tm.end();
@@ -501,7 +501,7 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, MULTI_TB);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, MULTI_TB + SCATTER_PAD);
     attr = true;
   }
   const Seg sg = {0u, n, (uint8_t)digit, SRC_REC, MODE_NONE, 0, 0};
@@ -518,9 +518,9 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   }
   int occ_s = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false>,
-                                                MULTI_SB, MULTI_TB);
+                                                MULTI_SB, MULTI_TB + SCATTER_PAD);
   const unsigned gs = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)n / T + 1, (size_t)ctx->sms * occ_s));
-  k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false><<<gs, MULTI_SB, MULTI_TB, st>>>(
+  k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false><<<gs, MULTI_SB, MULTI_TB + SCATTER_PAD, st>>>(
       v.L[0], v.tile_start, 1, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, nullptr, nullptr, nullptr, 0,
       v.splitc, v.probes, nullptr);
   RS_CUDA(cudaGetLastError());
