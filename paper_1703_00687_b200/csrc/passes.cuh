@@ -673,9 +673,26 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       }
       __syncthreads();
       RS_PROF(4);
-      for (uint32_t q = tid; q < m; q += SB) {
-        const Rec<R> x = ld_rec<R>(stage + (size_t)q * R);
-        st_rec<R>(dst + (size_t)(gofs[digit_of(key_of<R, K>(x), d)] + q) * R, x);
+      if constexpr (R == 32) {
+        // a lane pair moves one record, 16 bytes each: consecutive 16-byte smem
+        // reads (a lane per 32-byte record conflicts 2-way on every read); the
+        // key sits in the first half, its digit is passed to the partner lane
+        const int lane = tid & 31;
+        for (uint32_t h0 = 0; h0 < 2 * m; h0 += SB) {
+          const uint32_t h = h0 + (uint32_t)tid;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (h < 2 * m) v = reinterpret_cast<const uint4*>(stage)[h];
+          Rec<16> hr;
+          hr.a = v;
+          uint32_t dg = digit_of(key_of<16, K>(hr), d);
+          dg = __shfl_sync(0xffffffffu, dg, lane & ~1);
+          if (h < 2 * m) reinterpret_cast<uint4*>(dst + (size_t)(gofs[dg] + (h >> 1)) * R)[h & 1u] = v;
+        }
+      } else {
+        for (uint32_t q = tid; q < m; q += SB) {
+          const Rec<R> x = ld_rec<R>(stage + (size_t)q * R);
+          st_rec<R>(dst + (size_t)(gofs[digit_of(key_of<R, K>(x), d)] + q) * R, x);
+        }
       }
       moved += m;
       t = tn;
