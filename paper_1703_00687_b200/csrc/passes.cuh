@@ -968,7 +968,7 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* 
 // Steps 4-6 of the CTA-local sort, for a bin staged in smem in bucket order
 // (see k_local).  All threads of the CTA call it (it contains barriers).
 // Returns true when the tail sorter used the counter region as scratch.
-template <int R, int K, int LB, int NTW, bool PV = true>
+template <int R, int K, int LB, int NTW, bool PV = true, bool QT = false>
 __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* start16, uint32_t* blist, uint32_t cap,
                                              uint32_t n, uint32_t nbk, uint32_t d, uint32_t W, uint32_t ncol,
                                              uint32_t* s_nbig, TailScratch<K>* tsc, uint8_t* out, uint32_t off,
@@ -1038,9 +1038,9 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
     const uint32_t en = blist[cap - 1u - e];
     if (!(en >> 31)) continue;
     const uint32_t s0 = en & 0xffffu, c = (en >> 16) & 0x7fffu;
-    if (c <= TINY_MAX) {
+    if (!QT && c <= TINY_MAX) {
       warp_tail_sort<R, K, PV>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc[warp]);
-    } else if (lane == 0) {
+    } else if (lane == 0) {  // (QT: every mixed bucket; the caller's counters are live)
       Seg ns = {off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
       local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
       atomicMax(&ctl->max_local_len[nxt], c);
@@ -1332,33 +1332,39 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     for (int i = 0; i < IL; ++i)
       if ((uint32_t)(i * LB + tid) < qn) r[i] = ldg_rec<R>(src + (size_t)i * LB * R);
   };
+  // private ranks of this CTA's part of bin g (composite digit of width W(g))
+  constexpr int IP = (IL + 1) / 2;
+  uint32_t rk[IP];
+  auto count = [&](const Seg& g) {
+    const uint32_t pt = (g.len + CS - 1) / CS, q0 = min(g.len, crank * pt), qn = min(g.len, q0 + pt) - q0;
+    const uint32_t Wg = max(local_width(g.len, wmax), WMIN);
+#pragma unroll
+    for (int i = 0; i < IP; ++i) rk[i] = 0;
+#pragma unroll
+    for (int i = 0; i < IL; ++i) {
+      if ((uint32_t)(i * LB + tid) < qn) {
+        const uint32_t b = bucket_of(key_of<R, K>(r[i]), g.depth, Wg), sh = 16u * (b & 1u);
+        const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
+        rk[i >> 1] |= old << (16 * (i & 1));
+      }
+    }
+  };
+  // per bin: [owner scan] #B [stage] #C [count the next bin | finish this one] #A
   uint32_t bi = next_bin(blockIdx.x / CS);
   Seg sg;
   if (bi < nlist) {
     sg = list[bi];
     load(sg);
     prefetch_l2(next_bin(bi + ncl));
+    count(sg);
   }
+  cl.sync();  // #A: every CTA has counted
   bool pending = false;  // a bulk store still reads the stage
   while (bi < nlist) {
     const uint32_t n = sg.len, d = sg.depth;
     const uint32_t part = (n + CS - 1) / CS, p0 = min(n, crank * part), pn = min(n, p0 + part) - p0;
     const uint32_t W = max(local_width(n, wmax), WMIN);
     const uint32_t Wl = W - LCS, slice = 1u << Wl;
-    // 1. private ranks
-    constexpr int IP = (IL + 1) / 2;
-    uint32_t rk[IP];
-#pragma unroll
-    for (int i = 0; i < IP; ++i) rk[i] = 0;
-#pragma unroll
-    for (int i = 0; i < IL; ++i) {
-      if ((uint32_t)(i * LB + tid) < pn) {
-        const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W), sh = 16u * (b & 1u);
-        const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
-        rk[i >> 1] |= old << (16 * (i & 1));
-      }
-    }
-    cl.sync();  // every CTA has counted
     RS_PROF(0);
     // 2. slice owner: totals, starts, collision list, per-CTA bases
     const uint32_t nch = slice / 8u, m = nch / LB, c0 = (uint32_t)tid * m;
@@ -1484,7 +1490,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
           sg = list[bi];
           load(sg);
           prefetch_l2(next_bin(bi + ncl));
+          count(sg);
         }
+        cl.sync();  // #A
         continue;
       }
     }
@@ -1508,26 +1516,30 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
       load(nsg);
       prefetch_l2(next_bin(nb + ncl));
     }
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // #C
     RS_PROF(2);
-    // 4. finish the slice
+    // the bases are consumed: zero the counters (the next bin is counted after this one is finished)
+    zero_cnt(2u << W);
+    // 4. finish the slice (mixed buckets of > ES records go to the next Local
+    // level: the tail sorter's scratch would alias the live counters)
     const bool fix = 8 * ((int)K - (int)d) > (int)W;
     uint8_t* out = recs + ((size_t)sg.off + off[crank]) * R;
     const bool bulk = mine && (((uintptr_t)out | ((uintptr_t)mine * R)) & 15u) == 0;
-    local_finish<R, K, LB, NTW, false>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice, d, W,
-                                fix ? s_np + s_n3 : 0u, &s_nbig, reinterpret_cast<TailScratch<K>*>(cnt), out,
-                                sg.off + off[crank], local_next, nxt, ctl, bulk
+    local_finish<R, K, LB, NW, false, true>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice, d,
+                                            W, fix ? s_np + s_n3 : 0u, &s_nbig, nullptr, out, sg.off + off[crank],
+                                            local_next, nxt, ctl, bulk
 #ifdef RADSORT_PHASE_PROF
-                                , pf + 4
+                                            , pf + 4
 #endif
     );
     pending = bulk;
     done += mine;
+    __syncthreads();  // counters zeroed by every thread
+    if (nb < nlist) count(nsg);
     __syncthreads();
     RS_PROF(3);
-    zero_cnt(2u << W);
     if (tid == 0) { s_ncol = 0; s_nbig = 0; s_np = 0; s_n3 = 0; }
-    __syncthreads();
+    cl.sync();  // #A: every CTA has counted the next bin (and finished this one)
     bi = nb;
     sg = nsg;
   }
