@@ -759,7 +759,8 @@ template <int R, int K>
 __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
                                                       Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
-                                                      unsigned long long* __restrict__ probes, uint32_t lcap) {
+                                                      unsigned long long* __restrict__ probes, uint32_t lmin,
+                                                      uint32_t lcap) {
   enum : uint8_t { C_NONE = 0, C_COPY = 1, C_ES = 2, C_TINY = 3 };
   extern __shared__ uint4 smem_raw[];
   __shared__ uint8_t cls[RADIX];
@@ -807,7 +808,7 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
       c = C_ES;
     } else if (len <= TINY_MAX) {
       c = C_TINY;
-    } else if (len <= lcap) {  // CTA-local sort (<= C) or cluster-local sort (<= lcap)
+    } else if (len <= C || (len >= lmin && len <= lcap)) {  // CTA-local sort, or cluster-local sort in [lmin, lcap]
       Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
       local_cur[atomicAdd(&ctl->n_local[cur], 1u)] = ns;
       atomicMax(&ctl->max_local_len[cur], len);

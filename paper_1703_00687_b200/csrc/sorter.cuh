@@ -47,6 +47,9 @@ struct Sorter {
   static constexpr int CL_ILMAX = R <= 8 ? 32 : (R <= 16 ? 16 : 8);  // register budget of the record array
   static constexpr uint32_t CCAP_SMEM = CL_STAGE_CAP / 5 * 4 * CS;       // 20 % slack for uneven bucket slices
   static constexpr uint32_t CCAP = CCAP_SMEM < (uint32_t)(CL_ILMAX * 512 * CS) ? CCAP_SMEM : CL_ILMAX * 512 * CS;
+  // smaller bins (C < n < CL_MIN) take a further radix level: below ~2.5 C the
+  // cluster's per-bin phases cost more than the pass they save (measured, R = 32)
+  static constexpr uint32_t CL_MIN = C * 5 / 2;
 
   template <int IL>
   static void launch_cluster_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
@@ -247,11 +250,11 @@ struct Sorter {
     Ctl* ctl = v.ctl;
     const size_t tiles_max = v.tiles_max;
 
-    // cluster-local sorting of bins above C: on for R >= 24 (where C is small
-    // and it replaces a full radix level; measured); RADSORT_CLUSTER=1
-    // forces it on, =0 off
+    // cluster-local sorting of bins of CL_MIN..CCAP records: on for R = 32, the
+    // one layout where it beats a further radix level (measured);
+    // RADSORT_CLUSTER=1 forces it on for every layout, =0 off
     const char* cl_env = getenv("RADSORT_CLUSTER");
-    const bool cluster_ok = cl_env ? cl_env[0] == '1' : R >= 24;
+    const bool cluster_ok = cl_env ? cl_env[0] == '1' : R == 32;
     int occ_s = 0, occ_h = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB, false>, SB, TB + SCATTER_PAD);
     const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
@@ -358,7 +361,7 @@ struct Sorter {
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
-                                                                  tmp, v.probes, cluster_ok ? CCAP : C);
+                                                                  tmp, v.probes, CL_MIN, cluster_ok ? CCAP : C);
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
         stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry

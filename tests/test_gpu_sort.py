@@ -252,11 +252,11 @@ def force_cluster(monkeypatch):
 
 @pytest.mark.parametrize("R,K", LAYOUTS)
 def test_cluster_local_bins(R, K, force_cluster):
-    # level-0 bins of ~2.5 C records (C < len <= the cluster capacity): sorted
+    # level-0 bins of ~2.8 C records (2.5 C <= len <= the cluster capacity): sorted
     # by the 4-CTA cluster local sort (k_local_cluster), with a ragged tail
     import paper_1703_00687_b200 as rs
 
-    n = 256 * (C_of(R) * 5 // 2) + 77
+    n = 256 * (C_of(R) * 14 // 5) + 77
     check(dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=R * 3 + K), K)
     assert rs.last_stats()["scatter_passes"] == 1  # every level-0 bin was sorted on chip
 
@@ -264,7 +264,7 @@ def test_cluster_local_bins(R, K, force_cluster):
 @pytest.mark.parametrize("R,K", [(16, 8), (32, 16)])
 def test_cluster_off_matches(R, K, monkeypatch):
     monkeypatch.setenv("RADSORT_CLUSTER", "0")
-    n = 256 * (C_of(R) * 5 // 2) + 77
+    n = 256 * (C_of(R) * 14 // 5) + 77
     check(dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=R * 5 + K), K)
 
 
@@ -277,7 +277,7 @@ def test_cluster_local_bins_handed_back(R, K, mode, force_cluster):
     # the bins back to the next level's Large list; "split_slices" (half the
     # records share digits 1-2 = 0x92 0x34, the rest digit 1 < 16) fits, leaving
     # one huge colliding bucket for the next Local level.  Exact in all cases.
-    n = 256 * (C_of(R) * 5 // 2) + 5
+    n = 256 * (C_of(R) * 14 // 5) + 5
     a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=11)
     w, t = _top_word(a, K)
     keep_top = np.uint64(0xFF00_00FF_FFFF_FFFF)
