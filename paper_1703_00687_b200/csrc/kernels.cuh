@@ -585,9 +585,69 @@ __device__ __forceinline__ void warp_tail_sort_e(const uint8_t* src, uint8_t* ou
   __syncwarp();
 }
 
+// Dominant-key fast path of the tail sorter (duplicate-heavy bins such as the
+// k-mer stream's: ~100 copies of one key plus a few variants).  Pivot = the
+// middle record's key; one ballot pass counts the records below / above it.
+// If at most 32 records differ from it, the pivot's copies go straight to
+// their final slots (order inside an equal-key run is free, R2), the
+// others are parked in the scratch and placed by enumeration sort among their
+// own side.  Returns false (nothing written) when the bin is not of that kind.
+template <int R, int K>
+__device__ __forceinline__ bool warp_tail_dominant(const uint8_t* src, uint8_t* out, uint32_t n, int lane,
+                                                   TailScratch<K>& ws) {
+  static_assert(32 * R <= sizeof(TailScratch<K>), "scratch holds 32 records");
+  const Key<K> pv = ld_key<R, K>(src + (size_t)(n / 2) * R);
+  uint32_t nlt = 0, ngt = 0;
+  for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+    const uint32_t j = j0 + (uint32_t)lane;
+    bool lt = false, gt = false;
+    if (j < n) {
+      const Key<K> k = ld_key<R, K>(src + (size_t)j * R);
+      lt = key_lt(k, pv);
+      gt = key_lt(pv, k);
+    }
+    nlt += (uint32_t)__popc(__ballot_sync(0xffffffffu, lt));
+    ngt += (uint32_t)__popc(__ballot_sync(0xffffffffu, gt));
+  }
+  const uint32_t m = nlt + ngt, neq = n - m;
+  if (m > 32 || neq < m) return false;
+  uint8_t* scr = reinterpret_cast<uint8_t*>(&ws);
+  const uint32_t below = (1u << lane) - 1u;
+  uint32_t plt = 0, pgt = 0, peq = 0;  // records of each class placed so far
+  for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+    const uint32_t j = j0 + (uint32_t)lane;
+    Rec<R> x;
+    int cls = 3;
+    if (j < n) {
+      x = ld_rec<R>(src + (size_t)j * R);
+      const Key<K> k = key_of<R, K>(x);
+      cls = key_lt(k, pv) ? 0 : (key_lt(pv, k) ? 2 : 1);
+    }
+    const uint32_t b0 = __ballot_sync(0xffffffffu, cls == 0), b1 = __ballot_sync(0xffffffffu, cls == 1),
+                   b2 = __ballot_sync(0xffffffffu, cls == 2);
+    if (cls == 0) st_rec<R>(scr + (size_t)(plt + __popc(b0 & below)) * R, x);
+    else if (cls == 2) st_rec<R>(scr + (size_t)(nlt + pgt + __popc(b2 & below)) * R, x);
+    else if (cls == 1) st_rec<R>(out + (size_t)(nlt + peq + __popc(b1 & below)) * R, x);
+    plt += __popc(b0);
+    pgt += __popc(b2);
+    peq += __popc(b1);
+  }
+  __syncwarp();
+  if ((uint32_t)lane < m) {  // ES among the records on the lane's side of the pivot
+    const bool lo = (uint32_t)lane < nlt;
+    const uint32_t g0 = lo ? 0u : nlt, gn = lo ? nlt : ngt, i = (uint32_t)lane - g0;
+    const Rec<R> x = ld_rec<R>(scr + (size_t)lane * R);
+    const uint32_t rk = es_rank<R, K>(scr + (size_t)g0 * R, gn, i, key_of<R, K>(x));
+    st_rec<R>(out + (size_t)((lo ? 0u : nlt + neq) + rk) * R, x);
+  }
+  __syncwarp();
+  return true;
+}
+
 template <int R, int K, bool PV = true>
 __device__ __forceinline__ void warp_tail_sort(const uint8_t* src, uint8_t* out, uint32_t n, uint32_t depth, int lane,
                                                TailScratch<K>& ws) {
+  if (PV && n > 32 && warp_tail_dominant<R, K>(src, out, n, lane, ws)) return;
   if (n <= 32) warp_tail_sort_e<R, K, 1, PV>(src, out, n, depth, lane, ws);
   else if (n <= 64) warp_tail_sort_e<R, K, 2, PV>(src, out, n, depth, lane, ws);
   else warp_tail_sort_e<R, K, 4, PV>(src, out, n, depth, lane, ws);
