@@ -1,10 +1,11 @@
 // radsort_unique_count: run-length "unique key + count" over sorted records --
 // the k-mer counting step the paper's sorter serves in KMC3 (PAPER.md:280-282
-// §4.2).  Three kernels over 4096-record tiles:
+// §4.2).  Kernels over 4096-record tiles:
 //   k_uc_count  run heads per tile (record i starts a run iff i == 0 or its key
-//               differs from record i-1's)
+//               differs from record i-1's) and the tile's head bitmask
 //   k_uc_scan   exclusive scan of the tile counts (one CTA)
-//   k_uc_write  the key and start index of every run, at its rank
+//   k_uc_write  the key and start index of every run, at its rank (reads the
+//               bitmask and the keys of the heads only)
 //   k_uc_len    run lengths from consecutive starts
 #include "sorter.cuh"
 
@@ -20,20 +21,26 @@ __device__ __forceinline__ bool uc_head(const uint8_t* recs, uint64_t i) {
 
 template <int R, int K>
 __global__ void __launch_bounds__(UC_B) k_uc_count(const uint8_t* __restrict__ recs, uint64_t n,
-                                                   uint32_t* __restrict__ tile_cnt) {
+                                                   uint32_t* __restrict__ tile_cnt, uint32_t* __restrict__ heads) {
+  // also writes the run-head bitmask of the tile (bit j of word j / 32: record
+  // t0 + j starts a run), so that k_uc_write does not read the keys again
   const uint64_t t0 = (uint64_t)blockIdx.x * UC_T;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t c = 0;
-  for (uint32_t j = threadIdx.x; j < UC_T; j += UC_B) {
-    const uint64_t i = t0 + j;
-    if (i < n) c += (uint32_t)uc_head<R, K>(recs, i);
+  for (uint32_t j0 = 0; j0 < UC_T; j0 += UC_B) {
+    const uint64_t i = t0 + j0 + threadIdx.x;
+    const bool h = i < n && uc_head<R, K>(recs, i);
+    const uint32_t b = __ballot_sync(0xffffffffu, h);
+    if (lane == 0) heads[(size_t)blockIdx.x * (UC_T / 32) + (j0 >> 5) + w] = b;
+    c += (uint32_t)h;
   }
   c = __reduce_add_sync(0xffffffffu, c);
   __shared__ uint32_t ws[UC_B / 32];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  if (lane == 0) ws[w] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t s = 0;
-    for (int w = 0; w < UC_B / 32; ++w) s += ws[w];
+    for (int q = 0; q < UC_B / 32; ++q) s += ws[q];
     tile_cnt[blockIdx.x] = s;
   }
 }
@@ -67,21 +74,18 @@ __global__ void __launch_bounds__(1024) k_uc_scan(const uint32_t* __restrict__ t
 }
 
 template <int R, int K>
-__global__ void __launch_bounds__(UC_B) k_uc_write(const uint8_t* __restrict__ recs, uint64_t n,
-                                                   const unsigned long long* __restrict__ tile_off,
-                                                   uint8_t* __restrict__ keys_out, uint32_t* __restrict__ starts) {
-  constexpr int PT = UC_T / UC_B;  // records per thread, contiguous
-  __shared__ uint32_t ws[UC_B / 32];
+__global__ void __launch_bounds__(UC_T / 32) k_uc_write(const uint8_t* __restrict__ recs,
+                                                        const unsigned long long* __restrict__ tile_off,
+                                                        const uint32_t* __restrict__ heads, uint8_t* __restrict__ keys_out,
+                                                        uint32_t* __restrict__ starts) {
+  // one thread per 32-record word of the tile's head bitmask: exclusive scan of
+  // the popcounts, then the key and start index of every head (the keys of
+  // run heads only are read: ~1 record in 40 on the k-mer stream)
+  constexpr int NT = UC_T / 32, NWP = NT / 32;
+  __shared__ uint32_t ws[NWP];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint64_t base = (uint64_t)blockIdx.x * UC_T + (uint64_t)tid * PT;
-  uint32_t flags = 0, c = 0;
-#pragma unroll
-  for (int j = 0; j < PT; ++j) {
-    const uint64_t i = base + j;
-    const bool h = i < n && uc_head<R, K>(recs, i);
-    flags |= (uint32_t)h << j;
-    c += (uint32_t)h;
-  }
+  uint32_t b = heads[(size_t)blockIdx.x * NT + tid];
+  const uint32_t c = (uint32_t)__popc(b);
   uint32_t x = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -93,9 +97,11 @@ __global__ void __launch_bounds__(UC_B) k_uc_write(const uint8_t* __restrict__ r
   uint32_t add = 0;
   for (int i = 0; i < w; ++i) add += ws[i];
   unsigned long long u = tile_off[blockIdx.x] + add + x - c;
-  for (int j = 0; j < PT; ++j) {
-    if (!((flags >> j) & 1u)) continue;
-    const uint64_t i = base + j;
+  const uint64_t base = (uint64_t)blockIdx.x * UC_T + (uint64_t)tid * 32;
+  while (b) {
+    const uint32_t q = (uint32_t)__ffs(b) - 1u;
+    b &= b - 1u;
+    const uint64_t i = base + q;
     const Key<K> k = ld_key<R, K>(recs + i * R);
     uint64_t* ko = reinterpret_cast<uint64_t*>(keys_out + u * K);
     ko[0] = k.w0;
@@ -118,17 +124,18 @@ radsort_status unique_t(Context* ctx, const uint8_t* recs, uint64_t n, uint8_t* 
   const uint32_t ntiles = (uint32_t)((n + UC_T - 1) / UC_T);
   workspace_acquire(ctx, st);
   radsort_status rs;
-  // tile counts | tile offsets | total, then the run starts (reusing the multi-GPU scratch buffers)
-  if ((rs = ensure(ctx->mlo, (size_t)ntiles * 4 + 16)) || (rs = ensure(ctx->mlt, (size_t)ntiles * 8 + 16)) ||
-      (rs = ensure(ctx->mle, (size_t)n * 4 + 16)))
+  // tile counts + head bitmasks | tile offsets | total, then the run starts (reusing the multi-GPU scratch buffers)
+  if ((rs = ensure(ctx->mlo, (size_t)ntiles * 4 + (size_t)ntiles * (UC_T / 8) + 16)) ||
+      (rs = ensure(ctx->mlt, (size_t)ntiles * 8 + 16)) || (rs = ensure(ctx->mle, (size_t)n * 4 + 16)))
     return rs;
   uint32_t* tile_cnt = (uint32_t*)ctx->mlo.p;
+  uint32_t* heads = tile_cnt + ntiles;
   unsigned long long* tile_off = (unsigned long long*)ctx->mlt.p;
   unsigned long long* total = tile_off + ntiles;
   uint32_t* starts = (uint32_t*)ctx->mle.p;
-  k_uc_count<R, K><<<ntiles, UC_B, 0, st>>>(recs, n, tile_cnt);
+  k_uc_count<R, K><<<ntiles, UC_B, 0, st>>>(recs, n, tile_cnt, heads);
   k_uc_scan<<<1, 1024, 0, st>>>(tile_cnt, ntiles, tile_off, total);
-  k_uc_write<R, K><<<ntiles, UC_B, 0, st>>>(recs, n, tile_off, keys_out, starts);
+  k_uc_write<R, K><<<ntiles, UC_T / 32, 0, st>>>(recs, tile_off, heads, keys_out, starts);
   k_uc_len<<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sms * 8), 256, 0, st>>>(starts, total, n,
                                                                                                  counts_out);
   RS_CUDA(cudaGetLastError());
