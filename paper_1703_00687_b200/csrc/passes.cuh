@@ -1121,6 +1121,11 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     uint32_t ones = 0;
     bool all_equal = false;
     __syncthreads();  // counters zero, flags reset
+    if (tid == 0) {  // the next bins' descriptors into L1 (read after staging / for the L2 prefetch)
+      const uint32_t p1 = bi + gridDim.x, p2 = p1 + gridDim.x;
+      if (p1 < nlist) asm volatile("prefetch.global.L1 [%0];" ::"l"(list + p1));
+      if (p2 < nlist) asm volatile("prefetch.global.L1 [%0];" ::"l"(list + p2));
+    }
     RS_PROF(7);
     for (;;) {  // one round unless the composite digit is constant over the bin
 #pragma unroll
