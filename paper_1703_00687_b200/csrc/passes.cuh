@@ -1371,6 +1371,11 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     const uint32_t part = (n + CS - 1) / CS, p0 = min(n, crank * part), pn = min(n, p0 + part) - p0;
     const uint32_t W = max(local_width(n, wmax), WMIN);
     const uint32_t Wl = W - LCS, slice = 1u << Wl;
+    if (tid == 0) {  // the next bins' descriptors into L1
+      const uint32_t p1 = bi + ncl, p2 = p1 + ncl;
+      if (p1 < nlist) asm volatile("prefetch.global.L1 [%0];" ::"l"(list + p1));
+      if (p2 < nlist) asm volatile("prefetch.global.L1 [%0];" ::"l"(list + p2));
+    }
     RS_PROF(0);
     // 2. slice owner: totals, starts, collision list, per-CTA bases
     const uint32_t nch = slice / 8u, m = nch / LB, c0 = (uint32_t)tid * m;
