@@ -55,7 +55,22 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (arrival time, csv line)
+        self.t0 = self.t1 = None
+
+    def start(self):
+        """Start nvidia-smi early (it needs ~0.1-0.5 s before its first line)."""
+        return self.__enter__()
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        """End of the timed region: short regions get the first sample after it."""
+        self.t1 = time.time()
+        deadline = self.t1 + 2.0
+        while self.proc and time.time() < deadline and not any(t >= self.t0 for t, _ in self.lines):
+            time.sleep(0.02)
 
     def __enter__(self):
         try:
@@ -70,7 +85,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -83,7 +98,12 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for t, ln in self.lines if self.t0 is None or self.t0 <= t <= (self.t1 or t)]
+        after = False
+        if not inside and self.t0 is not None:  # region shorter than the sampling period
+            later = [ln for t, ln in self.lines if t >= self.t0]
+            inside, after = later[:1], bool(later)
+        for ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -97,7 +117,10 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if after:
+            out["note"] = "timed region shorter than the 100 ms sampling period: first sample after it"
+        return out
 
 
 def workload_desc(name, c, n):
@@ -217,6 +240,7 @@ def run_radsort(args):
             return n
         return rs.sort_multi(rec, tmp, n, K)
 
+    clk = ClockSampler(local_rank).start()  # started early: nvidia-smi's first line takes a while
     # warm-up (the first one is also the verification run: sorted + same multiset)
     for w in range(max(args.warmup, 1)):
         restore()
@@ -227,6 +251,7 @@ def run_radsort(args):
             bad, first = verify.sorted_check(rec.data_ptr(), n_out, R, K)
             if bad or (world == 1 and verify.digest(rec.data_ptr(), n, R) != dig_in):
                 print(json.dumps({"error": f"verification failed: {bad} inversions (first at {first})"}), flush=True)
+                clk.__exit__()
                 return 1
 
     rs.set_timing(True)
@@ -236,7 +261,8 @@ def run_radsort(args):
     launches = 0
     step_ms = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    clk.mark_start()
+    try:
         for _ in range(args.steps):
             restore()
             torch.cuda.synchronize()
@@ -254,6 +280,9 @@ def run_radsort(args):
             for k, v in st["kernel_bytes"].items():
                 kern_bytes[k] = kern_bytes.get(k, 0) + v
             launches += sum(st["kernel_launches"].values()) + (4 if kmc else 0)
+    finally:
+        clk.mark_end()
+        clk.__exit__()
     rs.set_timing(False)
     total_ms = sum(step_ms)
     if world > 1:
