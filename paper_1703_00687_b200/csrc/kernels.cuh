@@ -56,6 +56,7 @@ struct Ctl {
   unsigned long long bins_large, bins_local, bins_tiny, bins_final;
   unsigned long long bins_split, rec_split;  // dominant-key three-way splits (segments, records of the key)
   uint32_t n_probe;                          // probe-key table entries used this sort
+  uint32_t n_local_small[2];                 // Local list entries of <= small_cap<R>() records (by parity)
   unsigned long long prof[16];  // phase cycle counters (RADSORT_PHASE_PROF builds only)
 };
 

@@ -28,6 +28,13 @@ static __global__ void k_tilemap(const uint32_t* __restrict__ tile_start, uint32
     tile_seg[t] = seg_of_tile(tile_start, nseg, t);
 }
 
+// Bins of up to small_cap<R>() records are sorted by 64-thread CTAs (<= 256
+// bytes of records per thread; Sorter::launch_local).
+template <int R>
+__host__ __device__ constexpr uint32_t small_cap() {
+  return 64u * (256 / R >= 16 ? 16u : (256 / R >= 8 ? 8u : 4u));
+}
+
 // -------------------------------------------------------------- k_init
 // Level-0 set-up: the whole input is one bin.  If it fits the CTA-local
 // sorter it goes straight to the Local list, otherwise it becomes the single
@@ -118,6 +125,7 @@ static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint3
     ctl->scatter_ticket = 0;
     ctl->n_large_next = 0;
     ctl->n_local[nxt] = 0;
+    ctl->n_local_small[nxt] = 0;
     ctl->max_local_len[nxt] = 0;
   }
 }
@@ -811,6 +819,7 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
     } else if (len <= C || (len >= lmin && len <= lcap)) {  // CTA-local sort, or cluster-local sort in [lmin, lcap]
       Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
       local_cur[atomicAdd(&ctl->n_local[cur], 1u)] = ns;
+      if (len <= small_cap<R>()) atomicAdd(&ctl->n_local_small[cur], 1u);
       atomicMax(&ctl->max_local_len[cur], len);
       atomicAdd(&ctl->bins_local, 1ull);
     } else {
@@ -1045,6 +1054,7 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
       Seg ns = {off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
       local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
       atomicMax(&ctl->max_local_len[nxt], c);
+      if (c <= small_cap<R>()) atomicAdd(&ctl->n_local_small[nxt], 1u);
     }
   }
 #ifdef RADSORT_PHASE_PROF
@@ -1056,7 +1066,8 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
 template <int R, int K, int IL, int LB>
 __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     k_local(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes, uint32_t cnt_bytes,
-            uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp) {
+            uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp, uint32_t lmin,
+            uint32_t lmax) {
   extern __shared__ uint4 smem_raw[];
   constexpr int KW = K / 8;
   constexpr int NW = LB / 32;
@@ -1069,7 +1080,11 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t C = local_capacity<R>();  // larger bins of the list belong to k_local_cluster
   uint32_t bi = blockIdx.x;
-  while (bi < nlist && list[bi].len > C) bi += gridDim.x;
+  auto skip = [&](uint32_t b) {  // bins of another launch: other size class, or k_local_cluster's (> C)
+    const uint32_t l = list[b].len;
+    return l > lmax || l < lmin;
+  };
+  while (bi < nlist && skip(bi)) bi += gridDim.x;
   if (bi >= nlist) return;
   auto zero_cnt = [&](uint32_t bytes) {
     uint4* c4 = reinterpret_cast<uint4*>(cnt);
@@ -1213,7 +1228,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     // registers are free: the next bin's loads overlap this bin's write-out;
     // the bin after next streams into L2
     uint32_t nb = bi + gridDim.x;
-    while (nb < nlist && list[nb].len > C) nb += gridDim.x;
+    while (nb < nlist && skip(nb)) nb += gridDim.x;
     Seg nsg = sg;
     if (nb < nlist) {
       nsg = list[nb];

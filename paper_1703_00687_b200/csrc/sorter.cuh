@@ -13,7 +13,8 @@ struct Sorter {
 
   template <int IL, int LB>
   static void launch_local_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
-                             uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+                             uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms, uint32_t lmin = 0,
+                             uint32_t lmax = C) {
     // smem: staged bin | 2^W u16 counters (aliased by the tail sorter's per-warp
     // scratch) | list of the buckets holding >= 2 records
     const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
@@ -34,7 +35,7 @@ struct Sorter {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
     k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt,
-                                               ctl, recs, tmp);
+                                               ctl, recs, tmp, lmin, lmax);
   }
 
   // ---- cluster-local sort (bins of C < n <= CCAP records, k_local_cluster)
@@ -113,17 +114,31 @@ struct Sorter {
   // need 512 threads.
   // Returns true when a cluster launch may have handed bins to the next level's Large list.
   static bool launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
-                           Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
-    if (maxlen > C) {  // the list holds cluster-size bins: k_local takes the rest at full capacity
-      launch_local_t<(int)((C + 511) / 512), 512>(nloc, C, list, next, nxt, ctl, recs, tmp, st, sms);
-      launch_cluster(nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st, sms);
-      return true;
-    }
+                           Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms, uint32_t nsmall,
+                           int& nl) {
+    nl = 1;
     // small bins (up to 256 B of records per thread at 64 threads): 64-thread
     // CTAs, so that many bins are in flight per SM (the per-bin phases are
-    // latency-bound)
+    // latency-bound).  A list whose largest bin needs a bigger
+    // configuration but which holds at least one small bin per SM (counted by
+    // k_children / the tail queue) is split by size: its small bins run first
+    // in 64-thread CTAs, the bigger configuration then skips them.
     constexpr int ILS = 256 / R >= 16 ? 16 : (256 / R >= 8 ? 8 : 4);
-    if (maxlen <= (uint32_t)(64 * ILS)) {
+    constexpr uint32_t SMALL = small_cap<R>();
+    static_assert(SMALL == 64u * (uint32_t)ILS, "small_cap");
+    uint32_t lo = 0;
+    if (maxlen > SMALL && nsmall >= (uint32_t)sms && small_split()) {
+      launch_local_t<ILS, 64>(nloc, SMALL, list, next, nxt, ctl, recs, tmp, st, sms, 0, SMALL);
+      lo = SMALL + 1;
+      ++nl;
+    }
+    if (maxlen > C) {  // the list holds cluster-size bins: k_local takes the rest at full capacity
+      launch_local_t<(int)((C + 511) / 512), 512>(nloc, C, list, next, nxt, ctl, recs, tmp, st, sms, lo, C);
+      launch_cluster(nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st, sms);
+      ++nl;
+      return true;
+    }
+    if (maxlen <= SMALL) {
       const uint32_t il = (maxlen + 63) / 64;
 #define RS_LOCAL_S(IL) launch_local_t<IL, 64>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms)
       if (il <= 2) RS_LOCAL_S(2);
@@ -137,11 +152,11 @@ struct Sorter {
     }
     constexpr int ILMAX = (int)((C + 511) / 512);  // records per thread at 512 threads
     if ((size_t)maxlen > (size_t)256 * ILMAX) {
-      launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms);
+      launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms, lo, C);
       return false;
     }
     const uint32_t il = (maxlen + 255) / 256;
-#define RS_LOCAL(IL) launch_local_t<IL, 256>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms)
+#define RS_LOCAL(IL) launch_local_t<IL, 256>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms, lo, C)
     if (il <= 1) RS_LOCAL(1);
     else if (il <= 2) RS_LOCAL(2);
     else if (il <= 4) RS_LOCAL(4);
@@ -152,6 +167,15 @@ struct Sorter {
     else RS_LOCAL(ILMAX);
 #undef RS_LOCAL
     return false;
+  }
+
+  // size-split local launches (RADSORT_LOCAL_SPLIT=0 disables; measured)
+  static bool small_split() {
+    static const int on = [] {
+      const char* e = getenv("RADSORT_LOCAL_SPLIT");
+      return e ? atoi(e) : 1;
+    }();
+    return on != 0;
   }
 
   struct Views {
@@ -383,10 +407,11 @@ struct Sorter {
                 c.tiles_total, c.n_large_next, nloc, c.max_local_len[cur]);
       if (nloc) {
         tm.begin(RADSORT_K_LOCAL);
+        int nl = 1;
         const bool cl = launch_local(nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, L[nxt], ctl, recs, tmp, st,
-                                     ctx->sms);
+                                     ctx->sms, c.n_local_small[cur], nl);
         tm.end();
-        stats.kernel_launches[RADSORT_K_LOCAL] += cl ? 2 : 1;
+        stats.kernel_launches[RADSORT_K_LOCAL] += nl;
         RS_CUDA(cudaGetLastError());
         if (cl) {  // the cluster sort may have handed bins back as Large bins of the next level
           RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
