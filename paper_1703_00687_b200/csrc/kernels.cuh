@@ -57,6 +57,7 @@ struct Ctl {
   unsigned long long bins_split, rec_split;  // dominant-key three-way splits (segments, records of the key)
   uint32_t n_probe;                          // probe-key table entries used this sort
   uint32_t n_local_small[2];                 // Local list entries of <= small_cap<R>() records (by parity)
+  uint32_t n_local_med[2];                   // ... of small_cap < len <= med_cap<R>() records
   unsigned long long prof[16];  // phase cycle counters (RADSORT_PHASE_PROF builds only)
 };
 

@@ -34,6 +34,11 @@ template <int R>
 __host__ __device__ constexpr uint32_t small_cap() {
   return 64u * (256 / R >= 16 ? 16u : (256 / R >= 8 ? 8u : 4u));
 }
+// ... and bins of up to med_cap<R>() by 256-thread CTAs, two per SM (above it: 512 x 1)
+template <int R>
+__host__ __device__ constexpr uint32_t med_cap() {
+  return 256u * ((local_capacity<R>() + 511u) / 512u);
+}
 
 // -------------------------------------------------------------- k_init
 // Level-0 set-up: the whole input is one bin.  If it fits the CTA-local
@@ -126,6 +131,7 @@ static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint3
     ctl->n_large_next = 0;
     ctl->n_local[nxt] = 0;
     ctl->n_local_small[nxt] = 0;
+    ctl->n_local_med[nxt] = 0;
     ctl->max_local_len[nxt] = 0;
   }
 }
@@ -820,6 +826,7 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
       Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
       local_cur[atomicAdd(&ctl->n_local[cur], 1u)] = ns;
       if (len <= small_cap<R>()) atomicAdd(&ctl->n_local_small[cur], 1u);
+      else if (len <= med_cap<R>()) atomicAdd(&ctl->n_local_med[cur], 1u);
       atomicMax(&ctl->max_local_len[cur], len);
       atomicAdd(&ctl->bins_local, 1ull);
     } else {
@@ -1055,6 +1062,7 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
       local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
       atomicMax(&ctl->max_local_len[nxt], c);
       if (c <= small_cap<R>()) atomicAdd(&ctl->n_local_small[nxt], 1u);
+      else if (c <= med_cap<R>()) atomicAdd(&ctl->n_local_med[nxt], 1u);
     }
   }
 #ifdef RADSORT_PHASE_PROF

@@ -115,7 +115,7 @@ struct Sorter {
   // Returns true when a cluster launch may have handed bins to the next level's Large list.
   static bool launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
                            Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms, uint32_t nsmall,
-                           int& nl) {
+                           uint32_t nmed, int& nl) {
     nl = 1;
     // small bins (up to 256 B of records per thread at 64 threads): 64-thread
     // CTAs, so that many bins are in flight per SM (the per-bin phases are
@@ -151,7 +151,13 @@ struct Sorter {
       return false;
     }
     constexpr int ILMAX = (int)((C + 511) / 512);  // records per thread at 512 threads
+    static_assert(med_cap<R>() == 256u * (uint32_t)ILMAX, "med_cap");
     if ((size_t)maxlen > (size_t)256 * ILMAX) {
+      if (nmed >= (uint32_t)sms && small_split()) {  // the medium bins in 256-thread CTAs, two per SM
+        launch_local_t<ILMAX, 256>(nloc, med_cap<R>(), list, next, nxt, ctl, recs, tmp, st, sms, lo, med_cap<R>());
+        lo = med_cap<R>() + 1;
+        ++nl;
+      }
       launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms, lo, C);
       return false;
     }
@@ -409,7 +415,7 @@ struct Sorter {
         tm.begin(RADSORT_K_LOCAL);
         int nl = 1;
         const bool cl = launch_local(nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, L[nxt], ctl, recs, tmp, st,
-                                     ctx->sms, c.n_local_small[cur], nl);
+                                     ctx->sms, c.n_local_small[cur], c.n_local_med[cur], nl);
         tm.end();
         stats.kernel_launches[RADSORT_K_LOCAL] += nl;
         RS_CUDA(cudaGetLastError());
