@@ -177,11 +177,8 @@ struct Sorter {
 
   // size-split local launches (RADSORT_LOCAL_SPLIT=0 disables; measured)
   static bool small_split() {
-    static const int on = [] {
-      const char* e = getenv("RADSORT_LOCAL_SPLIT");
-      return e ? atoi(e) : 1;
-    }();
-    return on != 0;
+    const char* e = getenv("RADSORT_LOCAL_SPLIT");
+    return e ? atoi(e) != 0 : true;
   }
 
   struct Views {

@@ -309,3 +309,30 @@ def test_tail_sorter_dominant_key_pivot(R, K, per_bin):
     low = rng.integers(0, 256, n).astype(np.uint64)
     w[odd, 0] = (w[odd, 0] & ~np.uint64(0xFF)) | low[odd]
     check(a, K)
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 16), (32, 16)])
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("mix", ["small", "medium"])
+def test_local_size_classes(R, K, split, mix, monkeypatch):
+    # level-0 bins of two size classes, 160 of the smaller (more than one per
+    # SM) and 96 large ones (<= C): small (<= 64 x 256 B / R records) or medium
+    # (<= 256 x ceil(C / 512)) bins are then sorted by a launch of their own
+    # that the large configuration skips (RADSORT_LOCAL_SPLIT=0: one launch)
+    monkeypatch.setenv("RADSORT_LOCAL_SPLIT", split)
+    C = C_of(R)
+    small = {8: 1024, 16: 1024, 32: 512}[R]
+    med = 256 * ((C + 511) // 512)
+    lo = small // 2 if mix == "small" else (small + med) // 2
+    hi = (med + C) // 2 if mix == "medium" or R != 32 else (small + med) // 2
+    sizes = [lo if b % 8 < 5 else hi for b in range(256)]
+    n = int(sum(sizes))
+    a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=R + 5)
+    w, t = _top_word(a, K)
+    top = np.repeat(np.arange(256, dtype=np.uint64), sizes)
+    w[:, t] = (w[:, t] & np.uint64(0x00FF_FFFF_FFFF_FFFF)) | (top << np.uint64(56))
+    check(a, K)
+    import paper_1703_00687_b200 as rs
+
+    launches = rs.last_stats()["kernel_launches"]["local"]
+    assert launches == (2 if split == "1" else 1), launches
