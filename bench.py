@@ -10,10 +10,12 @@ copy (untimed; each step is bracketed by a barrier + cudaDeviceSynchronize and
 timed with CUDA events on the sort's stream).  Inputs (>= 3.2 GB at the
 default config) are larger than the 126 MB L2, so no L2 flush is needed.
 
-N = 1 runs the workload of BASELINE.json configs[1] (c2: 200M x 16 B records,
-8 B key < 2^40, payload = index) unless --config says otherwise.  N > 1
-(torchrun, one process per GPU, NCCL) runs radsort_sort_multi on a per-GPU
-shard of the same recipe (weak scaling: --config's n records per GPU).
+N = 1 runs the largest single-GPU configuration of BASELINE.json (c4: 1 B
+records of 32 B, 16-byte uniform keys, 16-byte payload; 32 GB) unless
+--config says otherwise.  N > 1 (torchrun, one process per GPU, NCCL) runs
+radsort_sort_multi: c3/c4 as BASELINE.json defines them, strong scaling (the
+config's n records in total, n/N per GPU); c5 weak scaling (n per GPU); c1/c2
+(single-GPU configs) weak.
 
 --impl reference times the CPU oracle (std::stable_sort, test infrastructure)
 on bounded samples of the same workload on the host cores; rank 0 only.
@@ -129,14 +131,15 @@ def workload_desc(name, c, n):
 
 
 def cpu_baseline(cfg_name, target_s=10.0, max_n=40_000_000):
-    """The oracle as it stands (single-threaded std::stable_sort) on a bounded
-    prefix sample of the workload; returns (Mrecords/s, sample description)."""
-    import numpy as np
-
+    """The oracle as it stands on a bounded prefix sample of the workload, on
+    the host cores: single-threaded std::stable_sort (oracle.sort), and its
+    all-cores form (oracle.sort_parallel: nproc chunks + merge rounds, the same
+    stable result).  Returns the cpu_baseline dict."""
     import oracle
     from datagen import host as dg
 
     c = dg.CONFIGS[cfg_name]
+    nproc = os.cpu_count() or 1
     n = 1_000_000
     a = dg.generate_config(cfg_name, n=n)
     t0 = time.perf_counter()
@@ -149,8 +152,22 @@ def cpu_baseline(cfg_name, target_s=10.0, max_n=40_000_000):
         oracle.sort(a, c["K"])
         dt = time.perf_counter() - t0
         n = n2
-    del np
-    return n / dt / 1e6, f"first {n} records of the {cfg_name} stream, oracle std::stable_sort, {dt:.2f} s"
+    t0 = time.perf_counter()
+    oracle.sort_parallel(a, c["K"], nproc)
+    dtp = time.perf_counter() - t0
+    sample = f"first {n} records of the {cfg_name} stream ({n * c['R'] / 1e9:.2f} GB)"
+    return {"value": round(n / dt / 1e6, 3), "unit": UNIT, "cores": 1, "nproc": nproc, "kind": "oracle",
+            "sample": f"{sample}, oracle std::stable_sort on 1 of {nproc} host cores, {dt:.2f} s",
+            "all_cores": {"value": round(n / dtp / 1e6, 3), "unit": UNIT, "cores": nproc,
+                          "kind": "oracle (all cores)",
+                          "sample": f"{sample}, {nproc} std::stable_sort chunks + std::merge rounds, {dtp:.2f} s"}}
+
+
+STRONG = ("c3", "c4")  # BASELINE.json: fixed total N over 1, 2, 4, 8 GPUs
+
+
+def scaling_of(cfg, world):
+    return "strong" if (cfg in STRONG and world > 1) else "weak"
 
 
 def run_reference(args):
@@ -177,9 +194,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "higher_is_better": True, "scaling": scaling_of(args.config, args.gpus), "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
         "config": {"workload": workload_desc(args.config, c, c["n"]), "sample_records_per_step": n},
-        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": 1, "nproc": os.cpu_count(), "kind": "oracle",
                          "sample": f"first {n} records of the {args.config} stream per step, std::stable_sort"},
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -204,17 +222,25 @@ def run_radsort(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     rs.init(local_rank)
     c = dict(dg.CONFIGS[args.config])
-    n = args.n or c["n"]
+    n_cfg = args.n or c["n"]
     R, K = c["R"], c["K"]
     stream = torch.cuda.current_stream()
+    strong = scaling_of(args.config, world) == "strong"
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # input shard of this rank: global record indices [rank*n, (rank+1)*n)
-    pristine = dd.generate_tensor(n, R, K, c["dist"], c["payload"], c["seed"], first=rank * n)
-    cap = n if world == 1 else int(n * 1.0) + 1024
+    # input shard of this rank: strong scaling splits the config's n records
+    # (global indices [first, first + n)); weak scaling gives every rank n
+    if strong:
+        first = n_cfg * rank // world
+        n = n_cfg * (rank + 1) // world - first
+    else:
+        first, n = rank * n_cfg, n_cfg
+    pristine = dd.generate_tensor(n, R, K, c["dist"], c["payload"], c["seed"], first=first)
+    # exact-balance output quotas differ from n by at most one record; slack for unequal shards
+    cap = n if world == 1 else n + world + 1024
     rec = torch.empty((cap, R), dtype=torch.uint8, device="cuda")
     tmp = torch.empty((cap, R), dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
@@ -290,7 +316,7 @@ def run_radsort(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     stats = rs.last_stats()
-    N_total = n * world
+    N_total = n_cfg if strong else n * world
     value = N_total * args.steps / (total_ms / 1e3) / 1e6
     passes_bytes = sum(kern_bytes.values()) / args.steps  # algorithmic bytes per step (read + write)
     eff_gbs = passes_bytes * world / (total_ms / args.steps / 1e3) / 1e9
@@ -343,15 +369,14 @@ def run_radsort(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sample = cpu_baseline(args.config)
-        cpu = {"value": round(v, 3), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+        cpu = cpu_baseline(args.config)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": workload_desc(args.config, c, n), "records_per_gpu": n, "rec_size": R,
+            "scaling": scaling_of(args.config, world), "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, c, N_total), "records_per_gpu": n, "rec_size": R,
                        "key_size": K, "parallelism": f"key-range sharding x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than the 126 MB L2; input restored from a pristine copy between steps"},
             "effective_hbm_gbs": round(eff_gbs, 1),
@@ -381,7 +406,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "kmc"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "kmc"])
     ap.add_argument("--n", type=int, default=0, help="override records per GPU")
     ap.add_argument("--impl", default="radsort", choices=["radsort", "reference"])
     ap.add_argument("--no-e2e", action="store_true")

@@ -81,8 +81,16 @@ typedef struct {
 
 /* Create the per-(process, device) context for `device` (cudaSetDevice is the
  * caller's business; this only records the device and queries its
- * attributes).  Idempotent.  Environment overrides (read here):
- * RADSORT_LOG=1 prints a per-level summary to stderr. */
+ * attributes).  Idempotent.  The context holds the sort's workspace: the bin
+ * lists of the recursion (§1 "bins that may be further processed
+ * independently in the recursive manner"; §3.1, the
+ * whole-array pass, then small bins, then tiny bins), the per-bin digit
+ * histograms and bin bases of each pass, and a small control block.
+ *   device   CUDA ordinal, 0 <= device < cudaGetDeviceCount(); else
+ *            RADSORT_ERR_INVALID_ARG (RADSORT_ERR_CUDA if CUDA is unusable).
+ * Ownership: the library owns the context until radsort_finalize.
+ * Environment overrides (read per sort): RADSORT_LOG=1 prints a per-level
+ * summary to stderr. */
 radsort_status radsort_init(int device);
 
 /* Sort n records in place in dev_records (§3.1 general scheme:
@@ -117,7 +125,13 @@ radsort_status radsort_sort_host(void* host_records, uint64_t n, uint32_t rec_si
                                  uint32_t key_size, void* stream);
 
 /* Multi-GPU collective sort (one process per GPU; every rank of nccl_comm
- * calls it with the same rec_size/key_size).  Input: dev_records[0..n_local).
+ * calls it with the same rec_size/key_size).  The paper's phase 1 -- "parallel
+ * processing of the whole array according to the first digit" (PAPER.md:119
+ * §3.1) -- carried across GPUs: the global top-digit histogram (allreduce)
+ * gives key-range splitters balanced by record count, one exchange sends every
+ * record to the rank owning its key range, and each rank then sorts its bins
+ * "independently in the recursive manner" (§1).
+ * Input: dev_records[0..n_local).
  * Output: dev_records[0..*n_out) holds this rank's key range; concatenating
  * the ranks' outputs in rank order equals radsort_sort of the concatenated
  * inputs (up to order inside equal-key runs).  Exact-balance quotas:
@@ -128,6 +142,24 @@ radsort_status radsort_sort_host(void* host_records, uint64_t n, uint32_t rec_si
 radsort_status radsort_sort_multi(void* dev_records, void* dev_tmp, uint64_t n_local,
                                   uint64_t capacity, uint64_t* n_out, uint32_t rec_size,
                                   uint32_t key_size, void* nccl_comm, void* stream);
+
+/* Communicator created by the library itself (instead of torch's
+ * ProcessGroupNCCL), so that the number of CTAs NCCL occupies during the
+ * exchange can be capped and the sort kernels keep the SMs.
+ *   radsort_comm_get_unique_id  rank 0 creates the 128-byte id (an
+ *                               ncclUniqueId) into id_out; the caller ships
+ *                               it to every rank (e.g. a torch broadcast).
+ *   radsort_comm_init           collective over nranks ranks; rank in
+ *                               [0, nranks); max_ctas = NCCL's maxCTAs
+ *                               (0 = NCCL's default).  *comm receives an
+ *                               ncclComm_t usable as radsort_sort_multi's
+ *                               nccl_comm, on the current device.
+ *   radsort_comm_destroy        frees it (after all work on it completed).
+ * Errors: NULL pointers / bad rank -> RADSORT_ERR_INVALID_ARG; NCCL failures
+ * -> RADSORT_ERR_NCCL with detail. */
+radsort_status radsort_comm_get_unique_id(void* id_out);
+radsort_status radsort_comm_init(const void* unique_id, int nranks, int rank, int max_ctas, void** comm);
+radsort_status radsort_comm_destroy(void* comm);
 
 /* In-process loopback transport for radsort_sort_multi (tests and emulation:
  * the build pool has one GPU per box).  G host threads act as the G ranks on
@@ -182,10 +214,11 @@ const char* radsort_version(void);
  * distinct key (key_size bytes, same little-endian layout as in a record) and
  * dev_counts_out[u] = its number of records, for u < *n_unique (host).  Both
  * output buffers must hold n entries (the worst case).  Work is ordered on
- * `stream`; the call returns after synchronizing it (to report *n_unique). */
+ * `stream` (a cudaStream_t passed as void*, NULL = legacy default stream); the
+ * call returns after synchronizing it (to report *n_unique). */
 radsort_status radsort_unique_count(const void* dev_sorted, uint64_t n, uint32_t rec_size, uint32_t key_size,
                                     void* dev_keys_out, uint32_t* dev_counts_out, uint64_t* n_unique,
-                                    cudaStream_t stream);
+                                    void* stream);
 
 /* Tiny-sorter benchmark (the GPU analog of PAPER.md:193-232 §4.1, Fig. 1;
  * benchmark infrastructure, not on the sort path): `bins` arrays of n

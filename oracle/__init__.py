@@ -8,6 +8,7 @@ Functions (each documented in oracle_sort.cpp with the PAPER.md / SPEC.md
 passage it follows):
 
 - ``sort(records, K)``            stable comparison sort on the K-byte key
+- ``sort_parallel(records, K, T)``  the same on T host cores (chunks + merge rounds; the all-cores CPU baseline)
 - ``digit(record, K, d)``         digit d (0 = most significant byte)
 - ``digit_hist(records, K, d)``   256-bin histogram of digit d
 - ``key_compare(a, b, K)``        -1 / 0 / +1
@@ -18,4 +19,4 @@ passage it follows):
 Pins: tests/test_oracle.py (brute force, numpy/lexsort special cases, SPEC
 worked examples in tests/golden/).  Parity pinned for every function above.
 """
-from .oracle import sort, digit, digit_hist, key_compare, compare, rank_bounds, unique_count, lib_path, build  # noqa: F401
+from .oracle import sort, sort_parallel, digit, digit_hist, key_compare, compare, rank_bounds, unique_count, lib_path, build  # noqa: F401

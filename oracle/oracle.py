@@ -20,7 +20,7 @@ def lib_path() -> str:
 def build(force: bool = False) -> str:
     """Compile liboracle.so (plain g++ -O2; no tuning -- it is the checker)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-pthread", "-shared", "-fPIC", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -32,6 +32,8 @@ def _load():
         vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
         L.oracle_sort.argtypes = [vp, vp, u64, u32, u32]
         L.oracle_sort.restype = ctypes.c_int
+        L.oracle_sort_parallel.argtypes = [vp, vp, u64, u32, u32, u32]
+        L.oracle_sort_parallel.restype = ctypes.c_int
         L.oracle_digit.argtypes = [vp, u32, u32]
         L.oracle_digit.restype = ctypes.c_int
         L.oracle_digit_hist.argtypes = [vp, u64, u32, u32, u32, vp]
@@ -59,6 +61,18 @@ def sort(records: np.ndarray, K: int) -> np.ndarray:
     rc = _load().oracle_sort(a.ctypes.data, out.ctypes.data, n, R, K)
     if rc != 0:
         raise ValueError(f"oracle_sort: invalid R={R} K={K}")
+    return out
+
+
+def sort_parallel(records: np.ndarray, K: int, threads: int | None = None) -> np.ndarray:
+    """sort() on `threads` host cores (chunked std::stable_sort + std::merge
+    rounds): byte-identical to sort().  The benchmark's all-cores CPU baseline."""
+    a = _as_records(records)
+    n, R = a.shape
+    out = np.empty_like(a)
+    t = threads or os.cpu_count() or 1
+    if _load().oracle_sort_parallel(a.ctypes.data, out.ctypes.data, n, R, K, t) != 0:
+        raise ValueError(f"oracle_sort_parallel: invalid R={R} K={K}")
     return out
 
 

@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <cstring>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -61,6 +62,47 @@ int oracle_sort(const uint8_t* in, uint8_t* out, uint64_t n, uint32_t R, uint32_
     return key_less(in + a * R, in + b * R, K);
   });
   for (uint64_t i = 0; i < n; ++i) std::memcpy(out + i * R, in + idx[i] * R, R);
+  return 0;
+}
+
+// The same stable sort on `threads` host cores (BASELINE.md §4 "all-cores
+// variant": the CPU baseline of the benchmark, not a parity reference): T
+// contiguous chunks are sorted by std::stable_sort in parallel, then merged in
+// ceil(log2 T) rounds of pairwise std::merge (parallel within a round).
+// std::merge takes from the left (earlier) range on ties, so the result is the
+// stable sort: byte-identical to oracle_sort.  Returns 0, or -1 on bad args.
+int oracle_sort_parallel(const uint8_t* in, uint8_t* out, uint64_t n, uint32_t R, uint32_t K, uint32_t threads) {
+  if (R == 0 || K == 0 || R % 8 || K % 8 || K > R || threads == 0) return -1;
+  const uint64_t T = std::max<uint64_t>(1, std::min<uint64_t>(threads, n / 1024 + 1));
+  auto less = [&](uint64_t a, uint64_t b) { return key_less(in + a * R, in + b * R, K); };
+  std::vector<uint64_t> idx(n), tmp(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::vector<uint64_t> bound(T + 1);
+  for (uint64_t t = 0; t <= T; ++t) bound[t] = n * t / T;
+  {
+    std::vector<std::thread> th;
+    for (uint64_t t = 0; t < T; ++t)
+      th.emplace_back([&, t] { std::stable_sort(idx.begin() + bound[t], idx.begin() + bound[t + 1], less); });
+    for (auto& x : th) x.join();
+  }
+  for (uint64_t width = 1; width < T; width *= 2) {  // runs of `width` chunks -> runs of 2*width
+    std::vector<std::thread> th;
+    for (uint64_t t = 0; t < T; t += 2 * width) {
+      const uint64_t a = bound[t], m = bound[std::min(T, t + width)], e = bound[std::min(T, t + 2 * width)];
+      th.emplace_back([&, a, m, e] {
+        std::merge(idx.begin() + a, idx.begin() + m, idx.begin() + m, idx.begin() + e, tmp.begin() + a, less);
+      });
+    }
+    for (auto& x : th) x.join();
+    idx.swap(tmp);
+  }
+  const uint64_t per = (n + T - 1) / T;
+  std::vector<std::thread> th;
+  for (uint64_t t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (uint64_t i = t * per; i < std::min(n, (t + 1) * per); ++i) std::memcpy(out + i * R, in + idx[i] * R, R);
+    });
+  for (auto& x : th) x.join();
   return 0;
 }
 

@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -41,6 +43,11 @@ struct Context {
   DevBuf large[2], local[2], hist, andor, segbase, tile_start, status, ctl, host_io[2];
   DevBuf splitc, probes;  // dominant-key split: per-segment class cursors; keys of the bins to fill
   DevBuf tile_seg;        // tile -> segment map of the current level
+  DevBuf tile_pre;        // reduce-then-scan per-tile digit prefixes (never aliases `status`)
+  // per-device launch state: kernels whose dynamic-smem attribute is set on this
+  // device, and the max active clusters of each cluster kernel on this device
+  std::set<const void*> smem_attr_set;
+  std::map<const void*, int> max_clusters;
   Ctl* h_ctl = nullptr;  // pinned
   uint32_t epoch = 0;
   cudaEvent_t ev[2 * 64] = {};
@@ -61,6 +68,15 @@ inline void workspace_release(Context* ctx, cudaStream_t st) {
 }
 
 radsort_status ensure(DevBuf& b, size_t bytes, bool zero = false);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (the attribute is per device; the context is per device and its mutex is
+// held by every sort).
+template <class F>
+inline void smem_attr(Context* ctx, F* f, int bytes) {
+  if (ctx->smem_attr_set.insert((const void*)f).second)
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 // per-kernel-class CUDA-event timing on the sort's stream (radsort_set_timing)
 struct Timer {

@@ -27,8 +27,10 @@
 // threads as ranks (tests, since the pool gives one GPU per box).
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <numeric>
+#include <thread>
 
 #include "driver.cuh"
 
@@ -102,8 +104,33 @@ struct NcclTransport : Transport {
   }
   int rank() const override { return r; }
   int size() const override { return g; }
+  // Wait for the stream's work without blocking inside the driver: a dead peer
+  // would leave an NCCL kernel spinning forever, so poll the stream and the
+  // communicator's asynchronous error state; give up after
+  // RADSORT_NCCL_TIMEOUT_S seconds (default 600).  On an error or a timeout the
+  // communicator is unusable: the caller aborts it (ncclCommAbort / torch).
   radsort_status check(cudaStream_t st) {
-    RS_CUDA(cudaStreamSynchronize(st));
+    const char* e = getenv("RADSORT_NCCL_TIMEOUT_S");
+    const double limit = e ? atof(e) : 600.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 0;; ++spin) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) {
+        set_detail("stream error during NCCL collective: %s", cudaGetErrorString(q));
+        return RADSORT_ERR_CUDA;
+      }
+      ncclResult_t ar = ncclSuccess;
+      if (ncclCommGetAsyncError(comm, &ar) != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+        set_detail("NCCL async error: %s", ncclGetErrorString(ar));
+        return RADSORT_ERR_NCCL;
+      }
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+        set_detail("NCCL collective did not complete within %.0f s (peer lost?)", limit);
+        return RADSORT_ERR_NCCL;
+      }
+      if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
     ncclResult_t ar = ncclSuccess;
     ncclCommGetAsyncError(comm, &ar);
     if (ar != ncclSuccess) {
@@ -134,9 +161,14 @@ struct NcclTransport : Transport {
   radsort_status exchange(const uint8_t* send, const std::vector<Msg>& sends, uint8_t* recv,
                           const std::vector<Msg>& recvs, cudaStream_t st) override {
     RS_NCCL(ncclGroupStart());
-    for (const Msg& m : sends) RS_NCCL(ncclSend(send + m.off, m.bytes, ncclUint8, m.peer, comm, st));
-    for (const Msg& m : recvs) RS_NCCL(ncclRecv(recv + m.off, m.bytes, ncclUint8, m.peer, comm, st));
-    RS_NCCL(ncclGroupEnd());
+    ncclResult_t r = ncclSuccess;  // the group is always closed, also when an enqueue fails
+    for (size_t i = 0; i < sends.size() && r == ncclSuccess; ++i)
+      r = ncclSend(send + sends[i].off, sends[i].bytes, ncclUint8, sends[i].peer, comm, st);
+    for (size_t i = 0; i < recvs.size() && r == ncclSuccess; ++i)
+      r = ncclRecv(recv + recvs[i].off, recvs[i].bytes, ncclUint8, recvs[i].peer, comm, st);
+    const ncclResult_t re = ncclGroupEnd();
+    RS_NCCL(r);
+    RS_NCCL(re);
     return check(st);
   }
 };
@@ -504,6 +536,39 @@ radsort_status radsort_sort_multi(void* dev_records, void* dev_tmp, uint64_t n_l
                                             rec_size, key_size, (cudaStream_t)stream, s);
   set_last_stats(s);
   return rs;
+}
+
+radsort_status radsort_comm_get_unique_id(void* id_out) {
+  if (!id_out) return RADSORT_ERR_INVALID_ARG;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  RS_NCCL(ncclGetUniqueId(&id));
+  memcpy(id_out, &id, sizeof id);
+  return RADSORT_OK;
+}
+
+radsort_status radsort_comm_init(const void* unique_id, int nranks, int rank, int max_ctas, void** comm) {
+  if (!unique_id || !comm || nranks < 1 || rank < 0 || rank >= nranks || max_ctas < 0) {
+    set_detail("radsort_comm_init: bad arguments");
+    return RADSORT_ERR_INVALID_ARG;
+  }
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof id);
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  if (max_ctas > 0) {
+    cfg.maxCTAs = max_ctas;
+    cfg.minCTAs = std::min(cfg.minCTAs > 0 ? cfg.minCTAs : 1, max_ctas);
+  }
+  ncclComm_t c = nullptr;
+  RS_NCCL(ncclCommInitRankConfig(&c, nranks, id, rank, &cfg));
+  *comm = c;
+  return RADSORT_OK;
+}
+
+radsort_status radsort_comm_destroy(void* comm) {
+  if (!comm) return RADSORT_ERR_INVALID_ARG;
+  RS_NCCL(ncclCommDestroy((ncclComm_t)comm));
+  return RADSORT_OK;
 }
 
 radsort_status radsort_loopback_create(int nranks, void** group) {

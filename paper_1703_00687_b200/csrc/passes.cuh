@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
                                                 uint32_t* __restrict__ segbase, Seg* large_next, Ctl* ctl,
                                                 uint32_t* __restrict__ splitc, int split_ok, int force = 0) {
   __shared__ uint32_t ws[8];
-  __shared__ int sh_const;
+  __shared__ int sh_const, sh_requeue;
   const uint32_t s = blockIdx.x;
   const int tid = threadIdx.x;
   const Seg sg = segs[s];
@@ -441,12 +441,37 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
     }
     return;
   }
-  if (tid == 0) sh_const = 0;
+  const unsigned long long* ao = andor + (size_t)s * 8;
+  if (tid == 0) {
+    sh_const = 0;
+    sh_requeue = 0;
+    // The digit a segment is histogrammed at must be its first non-constant
+    // one.  Bins below level 0 share their leading digits by construction; the
+    // level-0 depth is a guess from a strided sample (k_sample) that can be too
+    // deep when the sample misses a record differing in a higher digit.  The
+    // full-pass AND/OR decides: a segment with a non-constant digit above its
+    // depth is histogrammed again at that digit (one extra read, rare).
+    if (!force) {
+      uint64_t A[2], O[2];
+      for (int w = 0; w < K / 8; ++w) { A[w] = ~ao[w]; O[w] = ao[2 + w]; }
+      const uint32_t dt = first_nonconst_digit<K>(A, O, 0);
+      if (dt < (uint32_t)sg.depth) {
+        segs[s].mode = MODE_NONE;
+        Seg ns = sg;
+        ns.depth = (uint8_t)dt;
+        ns.mode = MODE_NONE;
+        ns.flags = (uint8_t)(sg.flags & ~FLAG_CAND);
+        large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+        atomicMin(&ctl->d0, dt);
+        sh_requeue = 1;
+      }
+    }
+  }
   __syncthreads();
+  if (sh_requeue) return;
   const uint32_t c = hist[(size_t)s * RADIX + tid];
   if (c == sg.len && !force) sh_const = 1;
   __syncthreads();
-  const unsigned long long* ao = andor + (size_t)s * 8;
   if (sh_const) {
     if (tid == 0) {
       uint64_t A[2], O[2];

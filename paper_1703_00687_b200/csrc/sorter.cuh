@@ -12,9 +12,10 @@ struct Sorter {
   static constexpr size_t LOCAL_SMEM_MAX = 227 * 1024 - 1024;  // dynamic smem ceiling per CTA (static smem aside)
 
   template <int IL, int LB>
-  static void launch_local_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
-                             uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms, uint32_t lmin = 0,
+  static void launch_local_t(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
+                             Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, uint32_t lmin = 0,
                              uint32_t lmax = C) {
+    const int sms = ctx->sms;
     // smem: staged bin | 2^W u16 counters (aliased by the tail sorter's per-warp
     // scratch) | list of the buckets holding >= 2 records
     const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
@@ -26,11 +27,7 @@ struct Sorter {
     while (wmax > LOCAL_WMIN && stage_bytes + cnt_of(wmax) + big_bytes > LOCAL_SMEM_MAX) --wmax;
     const size_t cnt_bytes = cnt_of(wmax);
     const size_t smem = stage_bytes + cnt_bytes + big_bytes;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_local<R, K, IL, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOCAL_SMEM_MAX);
-      attr = true;
-    }
+    smem_attr(ctx, k_local<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
@@ -53,19 +50,16 @@ struct Sorter {
   static constexpr uint32_t CL_MIN = C * 5 / 2;
 
   template <int IL>
-  static void launch_cluster_t(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
-                               Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+  static void launch_cluster_t(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
+                               Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
+    const int sms = ctx->sms;
     const uint32_t wmax = CL_W;
     const size_t stage_bytes = ((size_t)CL_STAGE_CAP * R + 15) & ~(size_t)15;
     const uint32_t cap = CL_STAGE_CAP / 2 + 1;
     const size_t smem = stage_bytes + CL_CNT + CL_SST + (((size_t)cap * 4 + 15) & ~(size_t)15);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_local_cluster<R, K, IL, 512, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)LOCAL_SMEM_MAX);
-      attr = true;
-    }
-    static int max_clusters = 0;
+    auto* kfn = k_local_cluster<R, K, IL, 512, CS>;
+    smem_attr(ctx, kfn, (int)LOCAL_SMEM_MAX);
+    int& max_clusters = ctx->max_clusters[(const void*)kfn];  // per device (the context's)
     if (!max_clusters) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(CS * sms / CS, 1, 1);
@@ -82,10 +76,10 @@ struct Sorter {
         list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)CL_CNT, cap, next, nxt, large_next, ctl, recs, tmp);
   }
 
-  static void launch_cluster(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
-                             Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms) {
+  static void launch_cluster(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
+                             Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
     const uint32_t il = (maxlen + CS * 512 - 1) / (CS * 512);  // records per thread
-#define RS_CL(IL) launch_cluster_t<IL>(nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st, sms)
+#define RS_CL(IL) launch_cluster_t<IL>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st)
     if (il <= 2) RS_CL(2);
     else if (il <= 4) RS_CL(4);
     else if constexpr (R <= 32) {
@@ -102,20 +96,16 @@ struct Sorter {
 #undef RS_CL
   }
 
-  static void set_attrs() {
-    static bool done = false;
-    if (done) return;
-    cudaFuncSetAttribute(k_children<R, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, CHILD_SCRATCH);
-    done = true;
-  }
+  static void set_attrs(Context* ctx) { smem_attr(ctx, k_children<R, K>, CHILD_SCRATCH); }
 
   // Local bins of up to `maxlen` records: IL records per thread, at most 256
   // bytes of records per thread; 256-thread CTAs (two per SM) unless the bins
   // need 512 threads.
   // Returns true when a cluster launch may have handed bins to the next level's Large list.
-  static bool launch_local(uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Seg* large_next,
-                           Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, int sms, uint32_t nsmall,
+  static bool launch_local(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
+                           Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, uint32_t nsmall,
                            uint32_t nmed, int& nl) {
+    const int sms = ctx->sms;
     nl = 1;
     // small bins (up to 256 B of records per thread at 64 threads): 64-thread
     // CTAs, so that many bins are in flight per SM (the per-bin phases are
@@ -128,19 +118,19 @@ struct Sorter {
     static_assert(SMALL == 64u * (uint32_t)ILS, "small_cap");
     uint32_t lo = 0;
     if (maxlen > SMALL && nsmall >= (uint32_t)sms && small_split()) {
-      launch_local_t<ILS, 64>(nloc, SMALL, list, next, nxt, ctl, recs, tmp, st, sms, 0, SMALL);
+      launch_local_t<ILS, 64>(ctx, nloc, SMALL, list, next, nxt, ctl, recs, tmp, st, 0, SMALL);
       lo = SMALL + 1;
       ++nl;
     }
     if (maxlen > C) {  // the list holds cluster-size bins: k_local takes the rest at full capacity
-      launch_local_t<(int)((C + 511) / 512), 512>(nloc, C, list, next, nxt, ctl, recs, tmp, st, sms, lo, C);
-      launch_cluster(nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st, sms);
+      launch_local_t<(int)((C + 511) / 512), 512>(ctx, nloc, C, list, next, nxt, ctl, recs, tmp, st, lo, C);
+      launch_cluster(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st);
       ++nl;
       return true;
     }
     if (maxlen <= SMALL) {
       const uint32_t il = (maxlen + 63) / 64;
-#define RS_LOCAL_S(IL) launch_local_t<IL, 64>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms)
+#define RS_LOCAL_S(IL) launch_local_t<IL, 64>(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st)
       if (il <= 2) RS_LOCAL_S(2);
       else if (il <= 4) RS_LOCAL_S(4);
       else if constexpr (ILS >= 8) {
@@ -154,15 +144,15 @@ struct Sorter {
     static_assert(med_cap<R>() == 256u * (uint32_t)ILMAX, "med_cap");
     if ((size_t)maxlen > (size_t)256 * ILMAX) {
       if (nmed >= (uint32_t)sms && small_split()) {  // the medium bins in 256-thread CTAs, two per SM
-        launch_local_t<ILMAX, 256>(nloc, med_cap<R>(), list, next, nxt, ctl, recs, tmp, st, sms, lo, med_cap<R>());
+        launch_local_t<ILMAX, 256>(ctx, nloc, med_cap<R>(), list, next, nxt, ctl, recs, tmp, st, lo, med_cap<R>());
         lo = med_cap<R>() + 1;
         ++nl;
       }
-      launch_local_t<ILMAX, 512>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms, lo, C);
+      launch_local_t<ILMAX, 512>(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, lo, C);
       return false;
     }
     const uint32_t il = (maxlen + 255) / 256;
-#define RS_LOCAL(IL) launch_local_t<IL, 256>(nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, sms, lo, C)
+#define RS_LOCAL(IL) launch_local_t<IL, 256>(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, lo, C)
     if (il <= 1) RS_LOCAL(1);
     else if (il <= 2) RS_LOCAL(2);
     else if (il <= 4) RS_LOCAL(4);
@@ -186,13 +176,16 @@ struct Sorter {
     Seg* Lo[2];
     uint32_t *hist, *segbase, *tile_start;
     unsigned long long *andor, *status, *probes;
-    uint32_t *splitc, *tile_seg;
+    uint32_t *splitc, *tile_seg, *tile_pre;
     Ctl* ctl;
     size_t tiles_max;
   };
 
   // Grow the workspace for n records and tiles of T records.
-  static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v) {
+  // lookback: the decoupled look-back status words (tiles x 256 u64) are
+  // needed (RADSORT_LOOKBACK=1, multi-GPU level-0 pass); otherwise the
+  // reduce-then-scan tile prefixes (tiles x 256 u32).
+  static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v, bool lookback = false) {
     const size_t capL = (size_t)n / C + 4;
     const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4;
     const size_t tiles_max = (size_t)n / T + capL + 4;
@@ -208,9 +201,13 @@ struct Sorter {
     if ((rs = ensure(ctx->probes, capL * 2 * sizeof(unsigned long long)))) return rs;
     if ((rs = ensure(ctx->tile_seg, tiles_max * sizeof(uint32_t)))) return rs;
     if ((rs = ensure(ctx->tile_start, (capL + 1) * sizeof(uint32_t)))) return rs;
-    const size_t old_status = ctx->status.bytes;
-    if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
-    if (ctx->status.bytes != old_status) ctx->epoch = 0;
+    if (lookback) {
+      const size_t old_status = ctx->status.bytes;
+      if ((rs = ensure(ctx->status, tiles_max * RADIX * sizeof(unsigned long long), true))) return rs;
+      if (ctx->status.bytes != old_status) ctx->epoch = 0;
+    } else {
+      if ((rs = ensure(ctx->tile_pre, tiles_max * RADIX * sizeof(uint32_t)))) return rs;
+    }
     if ((rs = ensure(ctx->ctl, sizeof(Ctl)))) return rs;
     if (!ctx->h_ctl) RS_CUDA(cudaMallocHost(&ctx->h_ctl, sizeof(Ctl)));
     v.L[0] = (Seg*)ctx->large[0].p;
@@ -225,6 +222,7 @@ struct Sorter {
     v.tile_seg = (uint32_t*)ctx->tile_seg.p;
     v.tile_start = (uint32_t*)ctx->tile_start.p;
     v.status = (unsigned long long*)ctx->status.p;
+    v.tile_pre = (uint32_t*)ctx->tile_pre.p;
     v.ctl = (Ctl*)ctx->ctl.p;
     v.tiles_max = tiles_max;
     return RADSORT_OK;
@@ -257,15 +255,12 @@ struct Sorter {
   static radsort_status run_cfg(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
                                 radsort_stats& stats, const Init* init) {
     constexpr uint32_t T = tile_recs<R, TB, SB>();
-    set_attrs();
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB + SCATTER_PAD);
-      cudaFuncSetAttribute(k_scatter<R, K, TB, SB, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB + SCATTER_PAD);
-      attr = true;
-    }
+    set_attrs(ctx);
+    smem_attr(ctx, k_scatter<R, K, TB, SB, MINB, false>, TB + SCATTER_PAD);
+    smem_attr(ctx, k_scatter<R, K, TB, SB, MINB, true>, TB + SCATTER_PAD);
+    const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
     Views v;
-    radsort_status rs = prepare(ctx, n, T, v);
+    radsort_status rs = prepare(ctx, n, T, v, !pre);
     if (rs) return rs;
     Seg** L = v.L;
     Seg** Lo = v.Lo;
@@ -284,10 +279,9 @@ struct Sorter {
     const bool cluster_ok = cl_env ? cl_env[0] == '1' : R == 32;
     int occ_s = 0, occ_h = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_scatter<R, K, TB, SB, MINB, false>, SB, TB + SCATTER_PAD);
-    const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
     const char* hg = getenv("RADSORT_HIST_CTAS_PER_SM");
     const unsigned hist_grid = (unsigned)ctx->sms * (hg ? atoi(hg) : 4);  // chunks of the reduce-then-scan prefix
-    uint32_t* tile_pre = (uint32_t*)status;               // tiles x 256 u32 (status is tiles x 256 u64)
+    uint32_t* tile_pre = v.tile_pre;                      // tiles x 256 u32 (its own buffer: never a stale status word)
     uint32_t* ch_first = (uint32_t*)ctx->mlo.p;
     uint32_t* ch_last = (uint32_t*)ctx->mhi.p;
     uint32_t* ch_tot = (uint32_t*)ctx->mlt.p;
@@ -371,7 +365,7 @@ struct Sorter {
         tm.begin(RADSORT_K_PLAN);
         k_plan<R, K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl, v.splitc, pre ? 1 : 0);
         tm.end();
-        if (++ctx->epoch >= 65536) {
+        if (!pre && ++ctx->epoch >= 65536) {  // look-back status words are epoch-tagged, never cleared
           RS_CUDA(cudaMemsetAsync(status, 0, ctx->status.bytes, st));
           ctx->epoch = 1;
         }
@@ -411,8 +405,8 @@ struct Sorter {
       if (nloc) {
         tm.begin(RADSORT_K_LOCAL);
         int nl = 1;
-        const bool cl = launch_local(nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, L[nxt], ctl, recs, tmp, st,
-                                     ctx->sms, c.n_local_small[cur], c.n_local_med[cur], nl);
+        const bool cl = launch_local(ctx, nloc, c.max_local_len[cur], Lo[cur], Lo[nxt], nxt, L[nxt], ctl, recs, tmp,
+                                     st, c.n_local_small[cur], c.n_local_med[cur], nl);
         tm.end();
         stats.kernel_launches[RADSORT_K_LOCAL] += nl;
         RS_CUDA(cudaGetLastError());
@@ -527,14 +521,9 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   if (n == 0) return RADSORT_OK;
   workspace_acquire(ctx, st);
   typename S::Views v;
-  radsort_status rs = S::prepare(ctx, n, T, v);
+  radsort_status rs = S::prepare(ctx, n, T, v, true);
   if (rs) return rs;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, MULTI_TB + SCATTER_PAD);
-    attr = true;
-  }
+  smem_attr(ctx, k_scatter<R, K, MULTI_TB, MULTI_SB, MULTI_MINB, false>, MULTI_TB + SCATTER_PAD);
   const Seg sg = {0u, n, (uint8_t)digit, SRC_REC, MODE_NONE, 0, 0};
   uint32_t h32[RADIX];
   for (int b = 0; b < RADIX; ++b) h32[b] = (uint32_t)h256[b];

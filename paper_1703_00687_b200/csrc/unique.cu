@@ -154,7 +154,8 @@ using namespace radsort;
 
 extern "C" radsort_status radsort_unique_count(const void* dev_sorted, uint64_t n, uint32_t rec_size,
                                                uint32_t key_size, void* dev_keys_out, uint32_t* dev_counts_out,
-                                               uint64_t* n_unique, cudaStream_t stream) {
+                                               uint64_t* n_unique, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
   if (!n_unique) {
     set_detail("unique_count: n_unique must be non-NULL");
     return RADSORT_ERR_INVALID_ARG;

@@ -21,7 +21,7 @@ EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_mu
            "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
            "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
            "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench",
-           "radsort_unique_count"]
+           "radsort_unique_count", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy"]
 
 
 class Stats(ctypes.Structure):
@@ -73,7 +73,10 @@ def _load():
     L.radsort_plan_equal_split.argtypes = [vp, i32, u64, u64, vp]
     L.radsort_tinybench.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(ctypes.c_double)]
     L.radsort_unique_count.argtypes = [vp, u64, u32, u32, vp, vp, ctypes.POINTER(u64), vp]
-    for f in ("radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
+    L.radsort_comm_get_unique_id.argtypes = [vp]
+    L.radsort_comm_init.argtypes = [vp, i32, i32, i32, ctypes.POINTER(vp)]
+    L.radsort_comm_destroy.argtypes = [vp]
+    for f in ("radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
               "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
               "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split",
               "radsort_tinybench", "radsort_unique_count"):
@@ -145,6 +148,37 @@ def sort_multi(records, tmp, n_local: int, key_size: int, group=None, stream=Non
     group = group or dist.group.WORLD
     backend = group._get_backend(torch.device("cuda"))
     comm = backend._comm_ptr()
+    R = records.shape[1]
+    cap = min(records.shape[0], tmp.numel() * tmp.element_size() // R)
+    n_out = ctypes.c_uint64(0)
+    init(records.device.index)
+    _check(lib.radsort_sort_multi(ctypes.c_void_p(records.data_ptr()), ctypes.c_void_p(tmp.data_ptr()), n_local, cap,
+                                  ctypes.byref(n_out), R, key_size, ctypes.c_void_p(comm), _stream_ptr(stream)))
+    return int(n_out.value)
+
+
+def comm_unique_id() -> bytes:
+    """A new 128-byte NCCL unique id (call on one rank, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.radsort_comm_get_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(unique_id: bytes, nranks: int, rank: int, max_ctas: int = 0) -> int:
+    """A library-owned NCCL communicator (ncclComm_t as int) with NCCL's CTAs capped at max_ctas."""
+    assert len(unique_id) == 128
+    c = ctypes.c_void_p()
+    _check(lib.radsort_comm_init(ctypes.create_string_buffer(unique_id, 128), nranks, rank, max_ctas,
+                                 ctypes.byref(c)))
+    return int(c.value)
+
+
+def comm_destroy(comm: int) -> None:
+    _check(lib.radsort_comm_destroy(ctypes.c_void_p(comm)))
+
+
+def sort_multi_comm(records, tmp, n_local: int, key_size: int, comm: int, stream=None) -> int:
+    """radsort_sort_multi on a communicator from comm_init; returns this rank's n_out."""
     R = records.shape[1]
     cap = min(records.shape[0], tmp.numel() * tmp.element_size() // R)
     n_out = ctypes.c_uint64(0)

@@ -78,3 +78,51 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in txt.replace("oracle/", ""), f
+
+
+C99_CLIENT = r"""
+#include <stdio.h>
+#include <string.h>
+#include "radsort.h"
+
+int main(void) {
+  radsort_stats st;
+  uint64_t q[3];
+  const char* s = radsort_error_string(RADSORT_ERR_UNSUPPORTED);
+  if (!s || !strstr(s, "unsupported")) return 10;
+  /* layout checks come before any device work: no GPU needed */
+  if (radsort_sort(NULL, NULL, 10, 12, 8, NULL) != RADSORT_ERR_INVALID_ARG) return 11;
+  if (radsort_sort(NULL, NULL, 10, 48, 8, NULL) != RADSORT_ERR_UNSUPPORTED) return 12;
+  /* a valid layout with NULL buffers never returns OK (no device, or bad pointers) */
+  if (radsort_sort(NULL, NULL, 10, 8, 8, NULL) == RADSORT_OK) return 13;
+  if (radsort_plan_quotas(10, 3, q) != RADSORT_OK || q[0] != 4 || q[1] != 3 || q[2] != 3) return 14;
+  if (radsort_last_stats(&st) != RADSORT_OK) return 15;
+  if (radsort_comm_init(NULL, 1, 0, 0, NULL) != RADSORT_ERR_INVALID_ARG) return 16;
+  printf("%s\n", radsort_version());
+  radsort_finalize();
+  return 0;
+}
+"""
+
+
+@pytest.mark.parametrize("std", ["c99", "c11"])
+def test_header_compiles_as_plain_c_and_links(tmp_path, std):
+    """A plain C client (no CUDA headers) compiles against include/radsort.h,
+    links libradsort.so and calls the entry points that need no GPU."""
+    import subprocess
+
+    import paper_1703_00687_b200 as rs
+
+    src = tmp_path / "client.c"
+    src.write_text(C99_CLIENT)
+    exe = tmp_path / "client"
+    libdir = os.path.dirname(rs.LIB_PATH)
+    cc = subprocess.run(["gcc", f"-std={std}", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                         "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                         "-L", libdir, "-l:libradsort.so", f"-Wl,-rpath,{libdir}"],
+                        capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    run = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=60)
+    assert run.returncode == 0, (run.returncode, run.stdout, run.stderr)
+    assert "radsort" in run.stdout

@@ -336,3 +336,28 @@ def test_local_size_classes(R, K, split, mix, monkeypatch):
 
     launches = rs.last_stats()["kernel_launches"]["local"]
     assert launches == (2 if split == "1" else 1), launches
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (16, 16), (32, 16)])
+@pytest.mark.parametrize("dist", ["sorted", "reverse"])
+def test_level0_digit_guess_too_deep(R, K, dist):
+    """The level-0 digit is guessed from a strided sample (k_sample); when the
+    sample misses the only records that differ in a higher digit, k_plan must
+    re-histogram at the true first non-constant digit.  n = 2^16+1
+    and 2^24+1 sorted/reverse keys are such inputs (sampled max 65520 < 65536)."""
+    sizes = [65537, (1 << 24) + 1] if R == 8 else [65537]
+    for n in sizes:
+        check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=9), K)
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (32, 16)])
+def test_rare_wide_outliers(R, K):
+    # 32-bit ids plus a few keys far above them at positions the sample never sees
+    n = 1_000_003
+    a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=21)
+    w = a.view(np.uint64).reshape(n, R // 8)
+    hi = K // 8 - 1
+    w[:, hi] &= np.uint64(0xFFFFFFFF)
+    for i in (1, 4097, 500_001, n - 2):  # the sample stride here is n // 4096 = 244
+        w[i, hi] = np.uint64(1 << 63) | np.uint64(i)
+    check(a, K)

@@ -256,8 +256,31 @@ def test_kmer_stream_matches_its_definition():
         for i in (0, 1, 7, 63, 299):
             got = int.from_bytes(bytes(a[i, :K]), "little")
             assert got == _kmer_reference(11, i, K)
-        n_err = 0
-        b = dg.generate(20000, K, K, "kmer", seed=12)
-        # overlapping reads of a 2^22-base reference: some k-mers repeat
+        # unique keys + counts of a small stream against a Counter over the
+        # pure-Python keys (independent of the generator and of the oracle)
+        import collections
+
+        m = 1500
+        b = dg.generate(m, K, K, "kmer", seed=12)
+        want = collections.Counter(_kmer_reference(12, i, K) for i in range(m))
         keys, counts = oracle.unique_count(oracle.sort(b, K), K)
-        assert counts.max() >= 1 and len(keys) <= 20000
+        got = {int.from_bytes(bytes(k), "little"): int(c) for k, c in zip(keys, counts)}
+        assert got == dict(want)
+        # overlapping reads of a 2^22-base reference: ~48 repeated read positions
+        # among 20000 reads, so some k-mer occurs at least twice
+        big = dg.generate(20000, K, K, "kmer", seed=12)
+        _, counts = oracle.unique_count(oracle.sort(big, K), K)
+        assert counts.max() >= 2 and counts.sum() == 20000
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (32, 16)])
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_parallel_sort_is_the_stable_sort(R, K, threads):
+    # pinned to numpy's stable lexsort (key words, high first; ties by input
+    # position): the stable order is unique, so the bytes must match exactly
+    for dist, n in (("few", 20011), ("uniform", 50000), ("bytes", 7)):
+        a = dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=n)
+        w = a.view(np.uint64).reshape(n, R // 8)
+        order = np.lexsort(tuple([np.arange(n)] + [w[:, j] for j in range(K // 8)]))
+        got = oracle.sort_parallel(a, K, threads)
+        assert np.array_equal(got, a[order])
