@@ -15,6 +15,7 @@
 
 #include "../../include/radsort.h"
 #include "passes.cuh"
+#include "local2.cuh"
 
 namespace radsort {
 

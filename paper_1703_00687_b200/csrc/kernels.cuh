@@ -115,6 +115,27 @@ template <> __device__ __forceinline__ Rec<40> ldg_rec<40>(const uint8_t* p) {
   return {__ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(q + 3), __ldg(q + 4)};
 }
 
+// read-only 256-bit load for R = 32 (LDG.256: one request per 32-byte record);
+// other sizes as ldg_rec.  Used where it was measured (ptxas 12.9 crashes on
+// it in some kernels).
+template <int R> __device__ __forceinline__ Rec<R> ldg_wide(const uint8_t* p) { return ldg_rec<R>(p); }
+template <> __device__ __forceinline__ Rec<32> ldg_wide<32>(const uint8_t* p) {
+  Rec<32> r;
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.a.x), "=r"(r.a.y), "=r"(r.a.z), "=r"(r.a.w), "=r"(r.b.x), "=r"(r.b.y), "=r"(r.b.z), "=r"(r.b.w)
+               : "l"(p));
+  return r;
+}
+
+// store to GLOBAL memory (p must be a global address): R = 32 is one 256-bit
+// store (STG.256), other sizes as st_rec
+template <int R> __device__ __forceinline__ void stg_rec(uint8_t* p, const Rec<R>& r) { st_rec<R>(p, r); }
+template <> __device__ __forceinline__ void stg_rec<32>(uint8_t* p, const Rec<32>& r) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.a.x), "r"(r.a.y), "r"(r.a.z),
+               "r"(r.a.w), "r"(r.b.x), "r"(r.b.y), "r"(r.b.z), "r"(r.b.w)
+               : "memory");
+}
+
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return (uint64_t)lo | ((uint64_t)hi << 32); }
 
 // ---------------------------------------------------------------------- keys

@@ -1015,7 +1015,8 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
                                              uint32_t n, uint32_t nbk, uint32_t d, uint32_t W, uint32_t ncol,
                                              uint32_t* s_nbig, TailScratch<K>* tsc, uint8_t* out, uint32_t off,
                                              Seg* local_next, int nxt, Ctl* ctl, bool bulk = false,
-                                             unsigned long long* pfx = nullptr) {
+                                             unsigned long long* pfx = nullptr, int nd_force = -1,
+                                             uint8_t src_big = SRC_REC) {
   constexpr int NW = LB / 32;
   constexpr uint32_t ES = es_max<R>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1075,7 +1076,8 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
   if (!nbig) return false;
   if (bulk && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // tails overwrite their part
   __syncthreads();  // written out; counters dead: the tail sorter's scratch aliases them
-  const uint32_t nd = d + (W >= 16 ? 2u : 1u);  // digits shared by a bucket's keys
+  // digits shared by a bucket's keys (nd_force: the caller's bucket does not start at a digit boundary)
+  const uint32_t nd = nd_force >= 0 ? (uint32_t)nd_force : d + (W >= 16 ? 2u : 1u);
   for (uint32_t e = warp; e < nbig && warp < NTW; e += NTW) {
     const uint32_t en = blist[cap - 1u - e];
     if (!(en >> 31)) continue;
@@ -1083,7 +1085,7 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
     if (!QT && c <= TINY_MAX) {
       warp_tail_sort<R, K, PV>(stage + (size_t)s0 * R, out + (size_t)s0 * R, c, nd, lane, tsc[warp]);
     } else if (lane == 0) {  // (QT: every mixed bucket; the caller's counters are live)
-      Seg ns = {off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
+      Seg ns = {off + s0, c, (uint8_t)nd, src_big, MODE_NONE, 0, 0};
       local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
       atomicMax(&ctl->max_local_len[nxt], c);
       if (c <= small_cap<R>()) atomicAdd(&ctl->n_local_small[nxt], 1u);
@@ -1305,6 +1307,282 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #undef RS_PROF
 }
 
+// L2-coherent loads (.cg: the SM's L1 may hold lines of the bin read before
+// the cluster's other CTAs wrote them)
+template <int R> __device__ __forceinline__ Rec<R> ldcg_rec(const uint8_t* p);
+template <> __device__ __forceinline__ Rec<32> ldcg_rec<32>(const uint8_t* p) {
+  Rec<32> r;
+  asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.a.x), "=r"(r.a.y), "=r"(r.a.z), "=r"(r.a.w), "=r"(r.b.x), "=r"(r.b.y), "=r"(r.b.z), "=r"(r.b.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+template <> __device__ __forceinline__ Rec<16> ldcg_rec<16>(const uint8_t* p) { return {__ldcg(reinterpret_cast<const uint4*>(p))}; }
+template <> __device__ __forceinline__ Rec<8> ldcg_rec<8>(const uint8_t* p) { return {__ldcg(reinterpret_cast<const uint2*>(p))}; }
+template <> __device__ __forceinline__ Rec<24> ldcg_rec<24>(const uint8_t* p) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+  return {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2)};
+}
+template <> __device__ __forceinline__ Rec<40> ldcg_rec<40>(const uint8_t* p) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+  return {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4)};
+}
+
+template <int R, int K>
+__device__ __forceinline__ void cswap_rec(Rec<R>& a, Rec<R>& b) {
+  if (key_lt(key_of<R, K>(b), key_of<R, K>(a))) { const Rec<R> t = a; a = b; b = t; }
+}
+
+// Fix-up of the colliding buckets of a slice written straight to global memory
+// by the direct-write cluster sort (k_local_cluster<.., DW = true>): the
+// records of a bucket sit in [start, start + c) in arbitrary order.  Buckets of
+// 2..4 records are loaded whole (independent L2 loads), sorted by a
+// compare-exchange network and written back (§2.2 sorting
+// networks for the tiniest arrays); 5..ES by insertion sort in place
+// (the fix-up sorter); larger buckets holding several keys
+// become Local bins of the next level.  Every thread of the CTA calls it.
+template <int R, int K, int LB>
+__device__ __forceinline__ void global_fixup(uint8_t* out, const uint16_t* start16, uint32_t* blist, uint32_t n,
+                                             uint32_t nbk, uint32_t d, uint32_t W, uint32_t ncol, uint32_t* s_nbig,
+                                             uint32_t off, Seg* local_next, int nxt, Ctl* ctl) {
+  constexpr uint32_t ES = es_max<R>();
+  constexpr int NW = LB / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!ncol) return;
+  for (uint32_t e = tid; e < ncol; e += LB) {
+    const uint32_t b = blist[e];
+    const uint32_t s0 = start16[b], c = (b + 1 < nbk ? (uint32_t)start16[b + 1] : n) - s0;
+    uint8_t* base = out + (size_t)s0 * R;
+    if (c <= 4) {
+      Rec<R> x0 = ldcg_rec<R>(base), x1 = ldcg_rec<R>(base + R), x2, x3;
+      if (c > 2) x2 = ldcg_rec<R>(base + 2 * R);
+      if (c > 3) x3 = ldcg_rec<R>(base + 3 * R);
+      if (c == 2) {
+        if (key_lt(key_of<R, K>(x1), key_of<R, K>(x0))) { stg_rec<R>(base, x1); stg_rec<R>(base + R, x0); }
+      } else if (c == 3) {
+        cswap_rec<R, K>(x0, x1); cswap_rec<R, K>(x1, x2); cswap_rec<R, K>(x0, x1);
+        stg_rec<R>(base, x0); stg_rec<R>(base + R, x1); stg_rec<R>(base + 2 * R, x2);
+      } else {
+        cswap_rec<R, K>(x0, x1); cswap_rec<R, K>(x2, x3); cswap_rec<R, K>(x0, x2); cswap_rec<R, K>(x1, x3);
+        cswap_rec<R, K>(x1, x2);
+        stg_rec<R>(base, x0); stg_rec<R>(base + R, x1); stg_rec<R>(base + 2 * R, x2); stg_rec<R>(base + 3 * R, x3);
+      }
+    } else if (c <= ES) {
+      for (uint32_t i = 1; i < c; ++i) {
+        const Rec<R> x = ldcg_rec<R>(base + (size_t)i * R);
+        const Key<K> kx = key_of<R, K>(x);
+        int j = (int)i - 1;
+        for (; j >= 0; --j) {
+          const Rec<R> y = ldcg_rec<R>(base + (size_t)j * R);
+          if (!key_lt(kx, key_of<R, K>(y))) break;
+          stg_rec<R>(base + (size_t)(j + 1) * R, y);
+        }
+        stg_rec<R>(base + (size_t)(j + 1) * R, x);
+      }
+    } else {
+      blist[e] = s0 | (c << 16) | 0x80000000u;  // > ES: checked below
+      atomicAdd(s_nbig, 1u);
+    }
+  }
+  __syncthreads();
+  if (!*s_nbig) return;
+  // > ES records: one warp per bucket checks for a single key (final as it is,
+  // PAPER.md:38); several keys -> a Local bin of the next level
+  for (uint32_t e = warp; e < ncol; e += NW) {
+    const uint32_t en = blist[e];
+    if (!(en >> 31)) continue;
+    const uint32_t s0 = en & 0xffffu, c = (en >> 16) & 0x7fffu;
+    const Key<K> k0 = key_of<R, K>(ldcg_rec<R>(out + (size_t)s0 * R));
+    bool diff = false;
+    for (uint32_t j = s0 + lane; j < s0 + c; j += 32) diff |= !key_eq(key_of<R, K>(ldcg_rec<R>(out + (size_t)j * R)), k0);
+    if (__any_sync(0xffffffffu, diff) && lane == 0) {
+      const uint32_t nd = d + (W >= 16 ? 2u : 1u);
+      Seg ns = {off + s0, c, (uint8_t)nd, SRC_REC, MODE_NONE, 0, 0};
+      local_next[atomicAdd(&ctl->n_local[nxt], 1u)] = ns;
+      atomicMax(&ctl->max_local_len[nxt], c);
+      if (c <= small_cap<R>()) atomicAdd(&ctl->n_local_small[nxt], 1u);
+      else if (c <= med_cap<R>()) atomicAdd(&ctl->n_local_med[nxt], 1u);
+    }
+  }
+}
+
+// -------------------------------------------------------------- k_local_big
+// The CTA-local sort (k_local's steps 1-6) for the largest local bins (up to C
+// records, one bin per SM: its staging takes most of the shared memory),
+// written for occupancy: 1024 threads (32 warps to hide the latency of the
+// barrier-separated phases) with IL <= 16 records each, and no per-record
+// state kept between the phases besides the records themselves:
+//  1. count: one smem atomic per record on the composite-digit bucket; the
+//     record that finds one earlier record in its bucket lists it (buckets of
+//     >= 2 records are the only ones the fix-up visits);
+//  2. exclusive scan of the counters;
+//  3. stage: a second atomic per record on the scanned starts gives its slot
+//     (order inside a bucket is free: the fix-up sorts every bucket of >= 2
+//     records by full key); afterwards counter b holds the END of bucket b,
+//     i.e. the start of bucket b + 1, so bucket b spans [E[b-1], E[b]) with
+//     E[-1] = 0 (a zero word in front of the counters);
+//  4.-6. as k_local (local_finish): fix-up, one TMA bulk store of the bin,
+//     mixed buckets of > ES records queued as Local bins of the next level.
+// The whole bin landing in one bucket (constant leading digits) is checked
+// once per bin (the bucket of record 0 holding n records), not per record.
+template <int R, int K, int IL, int LB>
+__global__ void __launch_bounds__(LB, 1)
+    k_local_big(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes, uint32_t cnt_bytes,
+                uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp, uint32_t lmin,
+                uint32_t lmax) {
+  extern __shared__ uint4 smem_raw[];
+  constexpr int KW = K / 8;
+  constexpr int NW = LB / 32;
+  uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
+  uint32_t* zpad = reinterpret_cast<uint32_t*>(stage + stage_bytes);  // 16 zero bytes: E[-1] = 0
+  uint32_t* cnt = zpad + 4;                                             // 2^W u16 counters
+  uint32_t* blist = cnt + cnt_bytes / 4u;                               // buckets of >= 2 records
+  __shared__ uint32_t wsum[NW], s_ncol, s_nbig, s_const;
+  __shared__ unsigned long long sna[2], so[2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t bi = blockIdx.x;
+  auto skip = [&](uint32_t b) {
+    const uint32_t l = list[b].len;
+    return l > lmax || l < lmin;
+  };
+  while (bi < nlist && skip(bi)) bi += gridDim.x;
+  if (bi >= nlist) return;
+  auto zero_cnt = [&](uint32_t bytes) {
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (uint32_t i = tid; i < bytes / 16u; i += LB) c4[i] = make_uint4(0, 0, 0, 0);
+  };
+  Rec<R> r[IL];
+  auto load = [&](const Seg& g) {
+    const uint8_t* p = buf_of(g.src, recs, tmp) + ((size_t)g.off + tid) * R;
+    const int lim = (int)g.len - tid;
+#pragma unroll
+    for (int i = 0; i < IL; ++i)
+      if (i * LB < lim) r[i] = ldg_rec<R>(p + (size_t)i * LB * R);
+  };
+  auto prefetch_l2 = [&](uint32_t b) {
+    if (tid == 0 && b < nlist) {
+      const Seg g = list[b];
+      const uintptr_t s0 = (uintptr_t)(buf_of(g.src, recs, tmp) + (size_t)g.off * R);
+      const uintptr_t s1 = (s0 + 15) & ~(uintptr_t)15, e1 = (s0 + (size_t)g.len * R) & ~(uintptr_t)15;
+      if (e1 > s1) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s1), "r"((uint32_t)(e1 - s1)) : "memory");
+    }
+  };
+  Seg sg = list[bi];
+  load(sg);
+  prefetch_l2(bi + gridDim.x);
+  zero_cnt(cnt_bytes);
+  if (tid < 4) zpad[tid] = 0;
+  if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+  if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
+  unsigned long long done = 0;
+  bool pending = false;  // a bulk store may still read the stage
+  for (;;) {
+    const uint32_t n = sg.len;
+    const int lim = (int)n - tid;
+    uint8_t* out = recs + (size_t)sg.off * R;
+    uint32_t d = sg.depth;
+    const uint32_t W = local_width(n, wmax);
+    bool all_equal = false;
+    __syncthreads();  // counters zero, flags reset
+    for (;;) {  // one round unless the composite digit is constant over the bin
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        if (i * LB < lim) {
+          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t sh = 16u * (b & 1u);
+          const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
+          if (old == 1u) blist[atomicAdd(&s_ncol, 1u)] = b;  // the bucket holds >= 2 records: list it once
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {  // the whole bin in one bucket?
+        const uint32_t b0 = bucket_of(key_of<R, K>(r[0]), d, W);
+        s_const = reinterpret_cast<const uint16_t*>(cnt)[b0] == n ? 1u : 0u;
+      }
+      local_scan<LB>(cnt, W, wsum);  // (its barrier also publishes s_const)
+      __syncthreads();
+      if (!s_const) break;
+      // every record in one bucket: skip the constant digits
+      uint64_t na[2] = {0, 0}, o[2] = {0, 0};
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        if (i * LB < lim) {
+          const Key<K> k = key_of<R, K>(r[i]);
+          na[0] |= ~k.w0; o[0] |= k.w0;
+          if constexpr (KW == 2) { na[1] |= ~k.w1; o[1] |= k.w1; }
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < KW; ++w) {
+        const uint32_t x0 = __reduce_or_sync(0xffffffffu, (uint32_t)na[w]);
+        const uint32_t x1 = __reduce_or_sync(0xffffffffu, (uint32_t)(na[w] >> 32));
+        const uint32_t y0 = __reduce_or_sync(0xffffffffu, (uint32_t)o[w]);
+        const uint32_t y1 = __reduce_or_sync(0xffffffffu, (uint32_t)(o[w] >> 32));
+        if (lane == 0) { atomicOr(&sna[w], u64of(x0, x1)); atomicOr(&so[w], u64of(y0, y1)); }
+      }
+      __syncthreads();
+      uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
+      const uint32_t d2 = first_nonconst_digit<K>(A, O, d);
+      __syncthreads();
+      zero_cnt(2u << W);
+      if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
+      if (tid == 0) { s_const = 0; s_ncol = 0; }
+      __syncthreads();
+      if (d2 >= (uint32_t)K) { all_equal = true; break; }
+      d = d2;
+    }
+    if (pending && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    pending = false;
+    __syncthreads();  // the previous bin's bulk store has read the stage
+    if (all_equal) {  // final where it is (copied out of tmp)
+      if (sg.src == SRC_TMP) {
+#pragma unroll
+        for (int i = 0; i < IL; ++i)
+          if (i * LB < lim) st_rec<R>(out + (size_t)(i * LB + tid) * R, r[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        if (i * LB < lim) {
+          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t sh = 16u * (b & 1u);
+          const uint32_t pos = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
+          st_rec<R>(stage + (size_t)pos * R, r[i]);
+        }
+      }
+    }
+    // registers are free: the next bin's loads overlap this bin's finish
+    uint32_t nb = bi + gridDim.x;
+    while (nb < nlist && skip(nb)) nb += gridDim.x;
+    Seg nsg = sg;
+    if (nb < nlist) {
+      nsg = list[nb];
+      load(nsg);
+    }
+    prefetch_l2(nb + gridDim.x);
+    if (!all_equal) {
+      const bool fix = 8 * ((int)K - (int)d) > (int)W;  // key bits left below the composite digit
+      __syncthreads();  // staged
+      const bool bulk = (((uintptr_t)out | ((uintptr_t)n * R)) & 15u) == 0;
+      // counters now hold bucket ends: start of bucket b = E[b - 1] (E[-1] = 0 in the pad)
+      local_finish<R, K, LB, NW, false, true>(stage, reinterpret_cast<const uint16_t*>(cnt) - 1, blist, cap, n,
+                                              1u << W, d, W, fix ? s_ncol : 0u, &s_nbig, nullptr, out, sg.off,
+                                              local_next, nxt, ctl, bulk);
+      pending = bulk;
+    }
+    done += n;
+    __syncthreads();
+    zero_cnt(2u << W);
+    if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
+    if (nb >= nlist) break;
+    bi = nb;
+    sg = nsg;
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid == 0) atomicAdd(&ctl->rec_local, done);
+}
+
 // -------------------------------------------------------------- k_local_cluster
 // The CTA-local sort for bins larger than one CTA's capacity C (up to about
 // CS * C): a cluster of CS CTAs sorts one bin (GPU analog of PAPER.md:134, the
@@ -1325,7 +1603,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 // digit is constant, is handed to the next level as a Large bin (nothing has
 // been written yet).  The next bin of each CTA is prefetched into L2 (TMA
 // bulk prefetch) while the current one is sorted.
-template <int R, int K, int IL, int LB, int CS>
+template <int R, int K, int IL, int LB, int CS, bool DW>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     k_local_cluster(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes,
                     uint32_t cnt_bytes, uint32_t cap, Seg* local_next, int nxt, Seg* large_next, Ctl* ctl,
@@ -1384,7 +1662,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     const uint8_t* src = buf_of(g.src, recs, tmp) + ((size_t)g.off + q0 + tid) * R;
 #pragma unroll
     for (int i = 0; i < IL; ++i)
-      if ((uint32_t)(i * LB + tid) < qn) r[i] = ldg_rec<R>(src + (size_t)i * LB * R);
+      if ((uint32_t)(i * LB + tid) < qn) r[i] = ldg_wide<R>(src + (size_t)i * LB * R);
   };
   // private ranks of this CTA's part of bin g (composite digit of width W(g))
   constexpr int IP = (IL + 1) / 2;
@@ -1531,7 +1809,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
       for (int o = 0; o < CS; ++o) {
         off[o] = run;
         run += s_tot[o];
-        over |= s_tot[o] > stage_cap;
+        over |= DW ? s_tot[o] == 0xffffffffu : s_tot[o] > stage_cap;  // DW: no staging, only a constant digit
       }
       mine = s_tot[crank];
       if (over) {  // skewed slices or a constant composite digit: the next level's Large list takes the bin
@@ -1555,14 +1833,29 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
         continue;
       }
     }
-    // 3. one remote store per record
+    if constexpr (DW) {
+      // 3'. every record straight to its place in the output (the whole bin is
+      // on chip in the cluster's registers, so writing over the input is safe):
+      // a 32-byte record is one full sector, the write needs no staging
+      uint8_t* bout = recs + (size_t)sg.off * R;
 #pragma unroll
-    for (int i = 0; i < IL; ++i) {
-      if ((uint32_t)(i * LB + tid) < pn) {
-        const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
-        const uint32_t pos = (uint32_t)cnt16[b] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-        const uint32_t o = b >> Wl;
-        st_rec<R>((o == crank ? stage : cl.map_shared_rank(stage, o)) + (size_t)pos * R, r[i]);
+      for (int i = 0; i < IL; ++i) {
+        if ((uint32_t)(i * LB + tid) < pn) {
+          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t pos = (uint32_t)cnt16[b] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+          stg_rec<R>(bout + (size_t)(off[b >> Wl] + pos) * R, r[i]);
+        }
+      }
+    } else {
+      // 3. one remote store per record
+#pragma unroll
+      for (int i = 0; i < IL; ++i) {
+        if ((uint32_t)(i * LB + tid) < pn) {
+          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t pos = (uint32_t)cnt16[b] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+          const uint32_t o = b >> Wl;
+          st_rec<R>((o == crank ? stage : cl.map_shared_rank(stage, o)) + (size_t)pos * R, r[i]);
+        }
       }
     }
     // staged (this CTA's slice complete): split cluster barrier; the next
@@ -1583,15 +1876,20 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     // level: the tail sorter's scratch would alias the live counters)
     const bool fix = 8 * ((int)K - (int)d) > (int)W;
     uint8_t* out = recs + ((size_t)sg.off + off[crank]) * R;
-    const bool bulk = mine && (((uintptr_t)out | ((uintptr_t)mine * R)) & 15u) == 0;
-    local_finish<R, K, LB, NW, false, true>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice, d,
-                                            W, fix ? s_np + s_n3 : 0u, &s_nbig, nullptr, out, sg.off + off[crank],
-                                            local_next, nxt, ctl, bulk
+    if constexpr (DW) {  // the slice's colliding buckets, in place in global memory (L2-resident)
+      global_fixup<R, K, LB>(out, reinterpret_cast<const uint16_t*>(sst), blist, mine, slice, d, W,
+                             fix ? s_np + s_n3 : 0u, &s_nbig, sg.off + off[crank], local_next, nxt, ctl);
+    } else {
+      const bool bulk = mine && (((uintptr_t)out | ((uintptr_t)mine * R)) & 15u) == 0;
+      local_finish<R, K, LB, NW, false, true>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice,
+                                              d, W, fix ? s_np + s_n3 : 0u, &s_nbig, nullptr, out,
+                                              sg.off + off[crank], local_next, nxt, ctl, bulk
 #ifdef RADSORT_PHASE_PROF
-                                            , pf + 4
+                                              , pf + 4
 #endif
-    );
-    pending = bulk;
+      );
+      pending = bulk;
+    }
     done += mine;
     __syncthreads();  // counters zeroed by every thread
     if (nb < nlist) count(nsg);

@@ -16,6 +16,8 @@ struct Sorter {
                              Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, uint32_t lmin = 0,
                              uint32_t lmax = C) {
     const int sms = ctx->sms;
+    lmax = std::min(lmax, ctx_local_hi);  // larger bins belong to k_local2
+    maxlen = std::min(maxlen, lmax);
     // smem: staged bin | 2^W u16 counters (aliased by the tail sorter's per-warp
     // scratch) | list of the buckets holding >= 2 records
     const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
@@ -35,6 +37,67 @@ struct Sorter {
                                                ctl, recs, tmp, lmin, lmax);
   }
 
+  // ---- the largest local bins: k_local_big (1024 threads, one bin per SM) with
+  // RADSORT_LOCAL_BIG=1; k_local at 512 threads otherwise
+  static bool big_on() {  // measured: c5 local 7.52 -> 7.22 ms, c3 5.23 -> 5.68 ms: opt-in
+    const char* e = getenv("RADSORT_LOCAL_BIG");
+    return e && e[0] == '1';
+  }
+  static void launch_big(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt, Ctl* ctl,
+                         uint8_t* recs, uint8_t* tmp, cudaStream_t st, uint32_t lmin, uint32_t lmax) {
+    constexpr int LB = 1024, IL = (int)((C + LB - 1) / LB);
+    lmax = std::min(lmax, ctx_local_hi);
+    maxlen = std::min(maxlen, lmax);
+    const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
+    const uint32_t cap = maxlen / 2 + 1;
+    const size_t big_bytes = ((size_t)cap * 4 + 15) & ~(size_t)15;
+    uint32_t wmax = local_width(maxlen, 16);
+    while (wmax > LOCAL_WMIN && stage_bytes + 16 + ((size_t)2 << wmax) + big_bytes > LOCAL_SMEM_MAX) --wmax;
+    const size_t cnt_bytes = (size_t)2 << wmax;
+    const size_t smem = stage_bytes + 16 + cnt_bytes + big_bytes;
+    auto* kfn = k_local_big<R, K, IL, LB>;
+    smem_attr(ctx, kfn, (int)LOCAL_SMEM_MAX);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, LB, smem);
+    const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)ctx->sms * std::max(occ, 1));
+    kfn<<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt, ctl, recs,
+                             tmp, lmin, lmax);
+  }
+
+  // ---- two-phase local sort (bins of local2_min() <= n <= local2_max<R>() records, k_local2)
+  static constexpr bool L2_BUILT = R == 8 || R == 16 || R == 32;  // off by default (RADSORT_LOCAL2=1): measured slower, DESIGN.md §3
+  static inline thread_local uint32_t ctx_local_hi = 0xffffffffu;  // the k_local launches' ceiling (set per launch_local)
+  // RADSORT_LOCAL2=0 disables it (the single-CTA and cluster sorts take the bins, as in round 1);
+  // RADSORT_LOCAL2_MIN sets the smallest bin it takes (default: 4096 records)
+  static uint32_t local2_min() {
+    if constexpr (!L2_BUILT) return 0xffffffffu;
+    const char* e = getenv("RADSORT_LOCAL2");
+    if (!e || e[0] != '1') return 0xffffffffu;
+    const char* m = getenv("RADSORT_LOCAL2_MIN");
+    return m ? (uint32_t)atoi(m) : 4096u;
+  }
+  static uint32_t local_max() {  // the largest bin the Local list takes
+    if constexpr (L2_BUILT) {
+      if (local2_min() != 0xffffffffu) return std::max(C, local2_max<R>());
+    }
+    return C;
+  }
+  static void launch_local2(Context* ctx, uint32_t nloc, const Seg* list, Seg* next, int nxt, Seg* large_next,
+                            Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st, uint32_t lmin) {
+    if constexpr (L2_BUILT) {
+      constexpr int LB = L2Cfg<R>::LB;
+      const size_t smem = local2_smem<R>();
+      smem_attr(ctx, k_local2<R, K>, (int)smem);
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local2<R, K>, LB, smem);
+      const char* e = getenv("RADSORT_DISCARD");
+      const int discard = e ? atoi(e) : 1;
+      const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)ctx->sms * std::max(occ, 1));
+      k_local2<R, K><<<g, LB, smem, st>>>(list, nloc, lmin, local2_max<R>(), next, nxt, large_next, ctl, recs, tmp,
+                                          discard);
+    }
+  }
+
   // ---- cluster-local sort (bins of C < n <= CCAP records, k_local_cluster)
   static constexpr int CS = 4;
   static constexpr uint32_t LCS = 2;
@@ -49,15 +112,26 @@ struct Sorter {
   // cluster's per-bin phases cost more than the pass they save (measured, R = 32)
   static constexpr uint32_t CL_MIN = C * 5 / 2;
 
-  template <int IL>
+  // DW (direct write): records go from the cluster's registers straight to
+  // their output slots (no shared-memory staging; a 32-byte record is one full
+  // sector, one STG.256), colliding buckets are fixed up in global memory.
+  // Measured on c4: direct writes 10.3 K vs DSMEM staging 14.6 K cycles per
+  // bin, but the global fix-up costs more than it saves (local 34.3 vs 32.7
+  // ms) -- off unless RADSORT_CLUSTER_DW=1 (R >= 24)
+  static bool cluster_dw() {
+    const char* e = getenv("RADSORT_CLUSTER_DW");
+    return R >= 24 && e && e[0] == '1';
+  }
+
+  template <int IL, bool DW>
   static void launch_cluster_t(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
                                Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
     const int sms = ctx->sms;
     const uint32_t wmax = CL_W;
-    const size_t stage_bytes = ((size_t)CL_STAGE_CAP * R + 15) & ~(size_t)15;
-    const uint32_t cap = CL_STAGE_CAP / 2 + 1;
+    const size_t stage_bytes = DW ? 0 : ((size_t)CL_STAGE_CAP * R + 15) & ~(size_t)15;
+    const uint32_t cap = DW ? CCAP / 2 + 1 : CL_STAGE_CAP / 2 + 1;
     const size_t smem = stage_bytes + CL_CNT + CL_SST + (((size_t)cap * 4 + 15) & ~(size_t)15);
-    auto* kfn = k_local_cluster<R, K, IL, 512, CS>;
+    auto* kfn = k_local_cluster<R, K, IL, 512, CS, DW>;
     smem_attr(ctx, kfn, (int)LOCAL_SMEM_MAX);
     int& max_clusters = ctx->max_clusters[(const void*)kfn];  // per device (the context's)
     if (!max_clusters) {
@@ -65,21 +139,25 @@ struct Sorter {
       cfg.gridDim = dim3(CS * sms / CS, 1, 1);
       cfg.blockDim = dim3(512, 1, 1);
       cfg.dynamicSmemBytes = LOCAL_SMEM_MAX;
-      if (cudaOccupancyMaxActiveClusters(&max_clusters, k_local_cluster<R, K, IL, 512, CS>, &cfg) != cudaSuccess ||
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kfn, &cfg) != cudaSuccess ||
           max_clusters <= 0) {
         cudaGetLastError();
         max_clusters = sms / CS;
       }
     }
     const unsigned clusters = (unsigned)std::max<size_t>(1, std::min<size_t>(nloc, (size_t)max_clusters));
-    k_local_cluster<R, K, IL, 512, CS><<<clusters * CS, 512, smem, st>>>(
+    kfn<<<clusters * CS, 512, smem, st>>>(
         list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)CL_CNT, cap, next, nxt, large_next, ctl, recs, tmp);
   }
 
   static void launch_cluster(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
                              Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
     const uint32_t il = (maxlen + CS * 512 - 1) / (CS * 512);  // records per thread
-#define RS_CL(IL) launch_cluster_t<IL>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st)
+#define RS_CL(IL)                                                                                       \
+  do {                                                                                                  \
+    if (cluster_dw()) launch_cluster_t<IL, true>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st); \
+    else launch_cluster_t<IL, false>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st); \
+  } while (0)
     if (il <= 2) RS_CL(2);
     else if (il <= 4) RS_CL(4);
     else if constexpr (R <= 32) {
@@ -107,6 +185,21 @@ struct Sorter {
                            uint32_t nmed, int& nl) {
     const int sms = ctx->sms;
     nl = 1;
+    ctx_local_hi = 0xffffffffu;
+    bool handed = false;
+    {
+      const uint32_t t2 = local2_min();
+      if (t2 != 0xffffffffu) {
+        if (maxlen >= t2) {  // the big bins: two-phase local sort (may hand groups back as Large bins)
+          launch_local2(ctx, nloc, list, next, nxt, large_next, ctl, recs, tmp, st, t2);
+          handed = true;
+          if (nloc == 0) return true;
+          ++nl;
+        }
+        ctx_local_hi = t2 - 1;
+        if (maxlen >= t2) maxlen = t2 - 1;
+      }
+    }
     // small bins (up to 256 B of records per thread at 64 threads): 64-thread
     // CTAs, so that many bins are in flight per SM (the per-bin phases are
     // latency-bound).  A list whose largest bin needs a bigger
@@ -123,7 +216,8 @@ struct Sorter {
       ++nl;
     }
     if (maxlen > C) {  // the list holds cluster-size bins: k_local takes the rest at full capacity
-      launch_local_t<(int)((C + 511) / 512), 512>(ctx, nloc, C, list, next, nxt, ctl, recs, tmp, st, lo, C);
+      if (big_on()) launch_big(ctx, nloc, C, list, next, nxt, ctl, recs, tmp, st, lo, C);
+      else launch_local_t<(int)((C + 511) / 512), 512>(ctx, nloc, C, list, next, nxt, ctl, recs, tmp, st, lo, C);
       launch_cluster(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st);
       ++nl;
       return true;
@@ -138,7 +232,7 @@ struct Sorter {
         else if constexpr (ILS >= 16) RS_LOCAL_S(16);
       }
 #undef RS_LOCAL_S
-      return false;
+      return handed;
     }
     constexpr int ILMAX = (int)((C + 511) / 512);  // records per thread at 512 threads
     static_assert(med_cap<R>() == 256u * (uint32_t)ILMAX, "med_cap");
@@ -148,8 +242,9 @@ struct Sorter {
         lo = med_cap<R>() + 1;
         ++nl;
       }
-      launch_local_t<ILMAX, 512>(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, lo, C);
-      return false;
+      if (big_on()) launch_big(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, lo, C);
+      else launch_local_t<ILMAX, 512>(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, lo, C);
+      return handed;
     }
     const uint32_t il = (maxlen + 255) / 256;
 #define RS_LOCAL(IL) launch_local_t<IL, 256>(ctx, nloc, maxlen, list, next, nxt, ctl, recs, tmp, st, lo, C)
@@ -162,7 +257,7 @@ struct Sorter {
     else if (il <= 16) RS_LOCAL(16);
     else RS_LOCAL(ILMAX);
 #undef RS_LOCAL
-    return false;
+    return handed;
   }
 
   // size-split local launches (RADSORT_LOCAL_SPLIT=0 disables; measured)
@@ -310,7 +405,7 @@ struct Sorter {
       for (uint32_t i = 0; i < init->nseg && init->depth < (uint32_t)K; ++i) {
         if (init->len[i] < 2) continue;
         const Seg sg = {init->off[i], init->len[i], (uint8_t)init->depth, SRC_REC, MODE_NONE, 0, 0};
-        if (init->len[i] > C) {
+        if (init->len[i] > local_max()) {
           lg.push_back(sg);
         } else {
           lc.push_back(sg);
@@ -382,7 +477,8 @@ struct Sorter {
         tm.end();
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
-                                                                  tmp, v.probes, CL_MIN, cluster_ok ? CCAP : C);
+                                                                  tmp, v.probes, local_max() > C ? C + 1 : CL_MIN,
+                                                                  local_max() > C ? local_max() : (cluster_ok ? CCAP : C));
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
         stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry

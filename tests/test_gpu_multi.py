@@ -121,3 +121,23 @@ def test_nccl_single_rank():
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def test_library_communicator_single_rank():
+    # radsort_comm_init (library-owned communicator, NCCL CTAs capped) drives
+    # the same collective sort
+    import paper_1703_00687_b200 as rs
+
+    uid = rs.comm_unique_id()
+    comm = rs.comm_init(uid, 1, 0, max_ctas=4)
+    try:
+        for R, K, dist in ((16, 8, "uniform40"), (8, 8, "zipf"), (32, 16, "uniform")):
+            a = dg.generate(250_000, R, K, dist, payload="index" if R > K else "random", seed=8)
+            rec = torch.from_numpy(a.copy()).cuda()
+            tmp = torch.empty_like(rec)
+            n_out = rs.sort_multi_comm(rec, tmp, a.shape[0], K, comm)
+            torch.cuda.synchronize()
+            assert n_out == a.shape[0]
+            assert oracle.compare(rec.cpu().numpy(), oracle.sort(a, K), K) == -1
+    finally:
+        rs.comm_destroy(comm)

@@ -268,15 +268,29 @@ def test_cluster_off_matches(R, K, monkeypatch):
     check(dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=R * 5 + K), K)
 
 
-@pytest.mark.parametrize("R,K", [(8, 8), (16, 16), (32, 16)])
+@pytest.mark.parametrize("R,K,dw", [(24, 8, "1"), (32, 16, "0"), (32, 8, "1"), (40, 16, "1")])
+def test_cluster_direct_write_variants(R, K, dw, force_cluster, monkeypatch):
+    # the direct-write cluster sort (records from registers straight to their
+    # output slots, colliding buckets fixed up in global memory) and the staged
+    # one, each on the layouts the other one is the default for
+    monkeypatch.setenv("RADSORT_CLUSTER_DW", dw)
+    n = 256 * (C_of(R) * 14 // 5) + 77
+    for dist in ("uniform", "few", "bytes"):
+        check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=R + K), K)
+
+
+@pytest.mark.parametrize("R,K,dw", [(8, 8, "0"), (16, 16, "0"), (32, 16, "1"), (32, 16, "0"), (24, 8, "1")])
 @pytest.mark.parametrize("mode", ["one_slice", "constant", "split_slices"])
-def test_cluster_local_bins_handed_back(R, K, mode, force_cluster):
+def test_cluster_local_bins_handed_back(R, K, dw, mode, force_cluster, monkeypatch):
     # the same bin sizes with a skewed digit 1: "one_slice" (digit 1 < 16: every
     # record of a bin lands in one CTA's bucket slice) and "constant" (digits
     # 1-2 constant: the composite digit is constant) make the cluster sort hand
     # the bins back to the next level's Large list; "split_slices" (half the
     # records share digits 1-2 = 0x92 0x34, the rest digit 1 < 16) fits, leaving
     # one huge colliding bucket for the next Local level.  Exact in all cases.
+    # (The direct-write variant, dw = 1, has no staging capacity: it sorts the
+    # "one_slice" bins itself.)
+    monkeypatch.setenv("RADSORT_CLUSTER_DW", dw)
     n = 256 * (C_of(R) * 14 // 5) + 5
     a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=11)
     w, t = _top_word(a, K)
@@ -361,3 +375,15 @@ def test_rare_wide_outliers(R, K):
     for i in (1, 4097, 500_001, n - 2):  # the sample stride here is n // 4096 = 244
         w[i, hi] = np.uint64(1 << 63) | np.uint64(i)
     check(a, K)
+
+
+@pytest.mark.parametrize("var", ["RADSORT_LOCAL_BIG", "RADSORT_LOCAL2"])
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (16, 16), (32, 16), (24, 8), (40, 16)])
+def test_opt_in_local_sorters(var, R, K, monkeypatch):
+    # the opt-in local sorters (k_local_big: 1024-thread CTAs, ranks by a second
+    # atomic pass; k_local2: two-phase partition through the scratch range) on
+    # bins of every size class, skewed and duplicate-heavy keys included
+    monkeypatch.setenv(var, "1")
+    for dist, n in (("uniform", 2_000_003), ("zipf", 1_500_001), ("few", 300_007), ("bytes", 700_001),
+                    ("uniform40", 1_000_003)):
+        check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=n % 97), K)

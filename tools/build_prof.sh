@@ -6,7 +6,8 @@ set -e
 cd "$(dirname "$0")/.."
 NCCL=$(python -c "import nvidia,os;print(os.path.join(nvidia.__path__[0],'nccl'))")
 mkdir -p build/prof scratch
-for f in radsort multi layout_16_8 layout_8_8 layout_16_16 layout_32_8 layout_32_16; do
+for u in paper_1703_00687_b200/csrc/*.cu; do
+  f=$(basename $u .cu)
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -DRADSORT_PHASE_PROF \
     -I "$NCCL/include" -c paper_1703_00687_b200/csrc/$f.cu -o build/prof/$f.o &
 done
