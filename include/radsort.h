@@ -233,6 +233,16 @@ radsort_status radsort_unique_count(const void* dev_sorted, uint64_t n, uint32_t
 radsort_status radsort_tinybench(uint32_t rec_size, uint32_t key_size, uint32_t n, uint32_t algo,
                                  uint64_t bins, double* ns_per_record);
 
+/* One tiny sorter of radsort_tinybench on caller-provided device arrays (test
+ * infrastructure for the sorters of PAPER.md:94-104 §2.2 / :159-183 §3.3):
+ * dev_in holds `bins` consecutive arrays of n records (2 <= n <= 128; algo 0:
+ * n <= 32), the keys of each array sharing their most significant byte (as
+ * every bin below the top level does); dev_out (same size, not overlapping)
+ * receives each array sorted by key.  Layouts as radsort_tinybench.  Ordered
+ * on `stream` (cudaStream_t as void*); returns after enqueueing. */
+radsort_status radsort_tinysort(uint32_t rec_size, uint32_t key_size, uint32_t n, uint32_t algo,
+                                const void* dev_in, void* dev_out, uint64_t bins, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -799,7 +799,7 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
                                                       Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
                                                       unsigned long long* __restrict__ probes, uint32_t lmin,
-                                                      uint32_t lcap) {
+                                                      uint32_t lcap, uint32_t bitonic_max) {
   enum : uint8_t { C_NONE = 0, C_COPY = 1, C_ES = 2, C_TINY = 3 };
   extern __shared__ uint4 smem_raw[];
   __shared__ uint8_t cls[RADIX];
@@ -889,6 +889,10 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
       }
       __syncwarp();
       if ((uint32_t)lane < len) st_rec<R>(out + (size_t)rank * R, x);
+      tiny_recs += len;
+      tiny_bins += 1;
+    } else if (len <= bitonic_max && d1 >= 1u) {  // the warp bitonic network (measured faster at 17..32, R <= 16)
+      warp_tiny_sort<R, K>(src, out, len, d1, lane);   // (gathers before it stores: in place is fine)
       tiny_recs += len;
       tiny_bins += 1;
     } else {

@@ -260,6 +260,17 @@ struct Sorter {
     return handed;
   }
 
+  // tiny bins of 17..32 records (R <= 16) are sorted by the warp bitonic network
+  // in k_children instead of the tail sorter: the tiny-sorter grid
+  // (profiles/r01_tinybench.txt) has it fastest there; end to end it is
+  // neutral on c3 / kmc.  RADSORT_TINY_BITONIC=n sets the
+  // ceiling (0 = tail sorter only; R <= 16, n <= 32)
+  static uint32_t bitonic_max() {
+    const char* e = getenv("RADSORT_TINY_BITONIC");
+    const uint32_t v = e ? (uint32_t)atoi(e) : 32u;
+    return R <= 16 ? std::min(v, 32u) : 0u;
+  }
+
   // size-split local launches (RADSORT_LOCAL_SPLIT=0 disables; measured)
   static bool small_split() {
     const char* e = getenv("RADSORT_LOCAL_SPLIT");
@@ -478,7 +489,8 @@ struct Sorter {
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
                                                                   tmp, v.probes, local_max() > C ? C + 1 : CL_MIN,
-                                                                  local_max() > C ? local_max() : (cluster_ok ? CCAP : C));
+                                                                  local_max() > C ? local_max() : (cluster_ok ? CCAP : C),
+                                                                  bitonic_max());
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
         stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry

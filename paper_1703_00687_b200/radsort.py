@@ -21,7 +21,8 @@ EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_mu
            "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
            "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
            "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench",
-           "radsort_unique_count", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy"]
+           "radsort_unique_count", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy",
+           "radsort_tinysort"]
 
 
 class Stats(ctypes.Structure):
@@ -73,10 +74,11 @@ def _load():
     L.radsort_plan_equal_split.argtypes = [vp, i32, u64, u64, vp]
     L.radsort_tinybench.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(ctypes.c_double)]
     L.radsort_unique_count.argtypes = [vp, u64, u32, u32, vp, vp, ctypes.POINTER(u64), vp]
+    L.radsort_tinysort.argtypes = [u32, u32, u32, u32, vp, vp, u64, vp]
     L.radsort_comm_get_unique_id.argtypes = [vp]
     L.radsort_comm_init.argtypes = [vp, i32, i32, i32, ctypes.POINTER(vp)]
     L.radsort_comm_destroy.argtypes = [vp]
-    for f in ("radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
+    for f in ("radsort_tinysort", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
               "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
               "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split",
               "radsort_tinybench", "radsort_unique_count"):
@@ -291,3 +293,17 @@ def unique_count(records, key_size: int, stream=None):
     _check(lib.radsort_unique_count(records.data_ptr(), n, R, key_size, keys.data_ptr(), counts.data_ptr(),
                                     ctypes.byref(out), st))
     return keys[:out.value], counts[:out.value]
+
+
+def tinysort(records, n: int, algo: int, key_size: int, stream=None):
+    """Sort consecutive arrays of n records (a CUDA uint8 tensor [bins * n, R],
+    keys of an array sharing their top byte) with tiny sorter `algo`; returns
+    the sorted copy (radsort_tinysort)."""
+    import torch
+
+    R = records.shape[1]
+    out = torch.empty_like(records)
+    bins = records.shape[0] // n
+    _check(lib.radsort_tinysort(R, key_size, n, algo, ctypes.c_void_p(records.data_ptr()),
+                                ctypes.c_void_p(out.data_ptr()), bins, _stream_ptr(stream)))
+    return out

@@ -201,6 +201,32 @@ def test_dominant_key_split_zipf_stats():
     assert st["bins_split"] >= 1
 
 
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (16, 16), (32, 8), (32, 16)])
+@pytest.mark.parametrize("algo", [0, 1, 2, 3])
+def test_tiny_sorters_match_oracle(R, K, algo):
+    # each tiny sorter of the tail (ES, warp bitonic network, warp tail sorter,
+    # insertion sort) against the oracle, array by array, on tie-heavy keys
+    # sharing their top byte (the sorters' contract: a bin below the top level)
+    import paper_1703_00687_b200 as rs
+
+    for n in (2, 3, 5, 16, 17, 31, 32, 33, 64, 100, 128):
+        if algo == 0 and n > 32:
+            continue
+        bins = 48
+        for dist in ("bytes", "few", "uniform"):
+            a = dg.generate(bins * n, R, K, dist, payload="index" if R > K else "random", seed=n * 7 + algo)
+            w = a.view(np.uint64).reshape(bins * n, R // 8)
+            hi = K // 8 - 1
+            w[:, hi] = (w[:, hi] & np.uint64(0x00FF_FFFF_FFFF_FFFF)) | np.uint64(0x4200_0000_0000_0000)
+            got = rs.tinysort(torch.from_numpy(a).cuda(), n, algo, K)
+            torch.cuda.synchronize()
+            g = got.cpu().numpy()
+            for b in range(bins):
+                seg = a[b * n:(b + 1) * n]
+                bad = oracle.compare(g[b * n:(b + 1) * n], oracle.sort(seg, K), K)
+                assert bad == -1, f"algo {algo} n {n} {dist} bin {b}: record {bad}"
+
+
 @pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (32, 16)])
 def test_tinybench_sorters_are_correct(R, K):
     # every tiny sorter sorts every array (the device check inside raises otherwise)
