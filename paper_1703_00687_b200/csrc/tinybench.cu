@@ -13,7 +13,7 @@
 //   3  insertion sort, one thread per bin (lane_insertion_sort)
 // Timed with CUDA events; the output is checked on the device (every bin
 // non-decreasing and a permutation of its input).  radsort_tinysort runs one
-// sorter on caller-provided arrays (its tests compare them with the oracle).
+// sorter on caller-provided arrays (for the tests of each sorter).
 // Benchmark / test infrastructure: not on the sort path.
 #include "sorter.cuh"
 
