@@ -77,6 +77,9 @@ typedef struct {
   uint64_t kernel_bytes[RADSORT_K_COUNT]; /* algorithmic HBM bytes (read + write)      */
   uint64_t bins_split;        /* segments split three ways around a dominant key        */
   uint64_t records_split;     /* records of those dominant keys (final after the split) */
+  uint32_t exchange;          /* multi-GPU: 1 = send/recv exchange, 2 = fused exchange
+                                 (next-digit scatter straight into the peers' buffers) */
+  uint32_t reserved_;
 } radsort_stats;
 
 /* Create the per-(process, device) context for `device` (cudaSetDevice is the

@@ -56,6 +56,7 @@ struct Context {
   cudaEvent_t done_ev = nullptr;  // workspace free once this event (last sort's stream) completes
   bool done_valid = false;
   DevBuf mprobe, mlo, mhi, mlt, mle;  // multi-GPU splitter search scratch
+  std::map<std::string, void*> ipc_open;  // peer buffers opened by CUDA IPC (handle bytes -> mapped base)
 };
 
 // Order `st` after the previous user of the workspace (another stream may still
@@ -130,6 +131,25 @@ template <int R, int K>
 radsort_status multi_bounds(Context* ctx, const uint8_t* buf, const uint32_t* lo, const uint32_t* hi,
                             const uint64_t* probes, uint32_t M, cudaStream_t st, uint64_t* lt, uint64_t* le);
 
+// Per-call workspace of the fused exchange (multi_piece_hist -> multi_piece_scatter).
+struct PieceWs {
+  DevBuf segs, tile_start, tile_seg, hist, andor, tile_pre, ch_first, ch_last, ch_tot, carry_in, ctl, segbase, dst;
+  uint32_t np = 0, hist_grid = 0;
+  size_t tiles = 0;
+  ~PieceWs() {
+    DevBuf* b[] = {&segs, &tile_start, &tile_seg, &hist, &andor, &tile_pre, &ch_first,
+                   &ch_last, &ch_tot, &carry_in, &ctl, &segbase, &dst};
+    for (DevBuf* x : b)
+      if (x->p) cudaFree(x->p);
+  }
+};
+template <int R, int K>
+radsort_status multi_piece_hist(Context* ctx, PieceWs& w, const uint8_t* src, const uint32_t* off,
+                                const uint32_t* len, uint32_t np, uint32_t digit, cudaStream_t st, uint32_t* h_hist);
+template <int R, int K>
+radsort_status multi_piece_scatter(Context* ctx, PieceWs& w, const uint8_t* src, const uint32_t* h_base,
+                                   const uint64_t* h_dst, cudaStream_t st);
+
 template <int R, int K>
 radsort_status run_layout_segs(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, const uint32_t* off,
                                const uint32_t* len, uint32_t nseg, uint32_t depth, cudaStream_t st, radsort_stats& s);
@@ -142,6 +162,9 @@ struct LayoutOps {
   radsort_status (*scatter)(Context*, uint8_t*, uint8_t*, uint32_t, uint32_t, const uint64_t*, cudaStream_t);
   radsort_status (*bounds)(Context*, const uint8_t*, const uint32_t*, const uint32_t*, const uint64_t*, uint32_t,
                            cudaStream_t, uint64_t*, uint64_t*);
+  radsort_status (*piece_hist)(Context*, PieceWs&, const uint8_t*, const uint32_t*, const uint32_t*, uint32_t, uint32_t,
+                               cudaStream_t, uint32_t*);
+  radsort_status (*piece_scatter)(Context*, PieceWs&, const uint8_t*, const uint32_t*, const uint64_t*, cudaStream_t);
 };
 // nullptr for layouts that are not built
 const LayoutOps* layout_ops(uint32_t R, uint32_t K);

@@ -11,4 +11,8 @@ template radsort_status multi_scatter<32, 16>(Context*, uint8_t*, uint8_t*, uint
                                               cudaStream_t);
 template radsort_status multi_bounds<32, 16>(Context*, const uint8_t*, const uint32_t*, const uint32_t*,
                                              const uint64_t*, uint32_t, cudaStream_t, uint64_t*, uint64_t*);
+template radsort_status multi_piece_hist<32, 16>(Context*, PieceWs&, const uint8_t*, const uint32_t*,
+                                                const uint32_t*, uint32_t, uint32_t, cudaStream_t, uint32_t*);
+template radsort_status multi_piece_scatter<32, 16>(Context*, PieceWs&, const uint8_t*, const uint32_t*,
+                                                   const uint64_t*, cudaStream_t);
 }

@@ -32,6 +32,8 @@
 #include <numeric>
 #include <thread>
 
+#include <unistd.h>
+
 #include "driver.cuh"
 
 namespace radsort {
@@ -80,6 +82,16 @@ struct Transport {
   // device data: every message of `sends` from `send`, every one of `recvs` into `recv`
   virtual radsort_status exchange(const uint8_t* send, const std::vector<Msg>& sends, uint8_t* recv,
                                   const std::vector<Msg>& recvs, cudaStream_t st) = 0;
+  // Peer access for the fused exchange: out[p] = rank p's `mine` (its record
+  // buffer) mapped into this process.  Collective; every rank gets the same
+  // answer: RADSORT_OK everywhere, or RADSORT_ERR_UNSUPPORTED everywhere (the
+  // caller then takes the send/recv exchange).
+  virtual radsort_status peer_bases(uint8_t* mine, std::vector<uint8_t*>& out, Context* ctx, cudaStream_t st) = 0;
+  radsort_status barrier(cudaStream_t st) {
+    const uint64_t one = 1;
+    uint64_t sum = 0;
+    return allreduce(&one, &sum, 1, ROp::Sum, st);
+  }
 };
 
 #define RS_NCCL(x)                                                                             \
@@ -171,6 +183,87 @@ struct NcclTransport : Transport {
     RS_NCCL(re);
     return check(st);
   }
+  // CUDA IPC: every rank exports the allocation holding its record buffer
+  // (cudaIpcGetMemHandle of the allocation base, found with the driver's
+  // cuMemGetAddressRange) and opens its peers' handles once per context (the
+  // mappings are cached until radsort_finalize).  Allocations IPC cannot export
+  // (e.g. VMM / expandable segments) make every rank fall back.
+  radsort_status peer_bases(uint8_t* mine, std::vector<uint8_t*>& out, Context* ctx, cudaStream_t st) override {
+    typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        get_range = (GetRange)fn;
+      cudaGetLastError();
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    uint64_t pay[13] = {};
+    unsigned long long base = 0;
+    size_t size = 0;
+    cudaIpcMemHandle_t h;
+    bool ok = mine && get_range && get_range(&base, &size, (unsigned long long)(uintptr_t)mine) == 0 &&
+              cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base) == cudaSuccess;
+    cudaGetLastError();
+    if (ok) memcpy(pay, &h, sizeof h);
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handle");
+    pay[8] = ok ? (uint64_t)(uintptr_t)mine - base : 0;
+    pay[9] = (uint64_t)getpid();
+    pay[10] = (uint64_t)dev;
+    pay[11] = ok ? 1 : 0;
+    pay[12] = (uint64_t)(uintptr_t)mine;
+    std::vector<uint64_t> all(13 * (size_t)g);
+    radsort_status rs;
+    if ((rs = allgather(pay, all.data(), 13, st))) return rs;
+    uint64_t okall = 1;
+    for (int p = 0; p < g; ++p) okall &= all[13 * (size_t)p + 11];
+    out.assign(g, nullptr);
+    uint64_t opened = okall;
+    std::unique_lock<std::mutex> lk(ctx->mu);  // the context's cache of opened handles
+    for (int p = 0; p < g && opened; ++p) {
+      const uint64_t* q = &all[13 * (size_t)p];
+      if (p == r) {
+        out[p] = mine;
+      } else if (q[9] == (uint64_t)getpid()) {  // same process (another device): the pointer itself
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, dev, (int)q[10]);
+        if (!can || ((cudaDeviceEnablePeerAccess((int)q[10], 0) != cudaSuccess) &&
+                     cudaGetLastError() != cudaErrorPeerAccessAlreadyEnabled))
+          opened = 0;
+        cudaGetLastError();
+        out[p] = (uint8_t*)(uintptr_t)q[12];
+      } else {
+        const std::string key((const char*)q, 64);
+        auto it = ctx->ipc_open.find(key);
+        void* ptr = nullptr;
+        if (it != ctx->ipc_open.end()) {
+          ptr = it->second;
+        } else {
+          cudaIpcMemHandle_t ph;
+          memcpy(&ph, q, sizeof ph);
+          if (cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+            ctx->ipc_open[key] = ptr;
+          } else {
+            cudaGetLastError();
+            ptr = nullptr;
+            opened = 0;
+          }
+        }
+        out[p] = ptr ? (uint8_t*)ptr + q[8] : nullptr;
+      }
+    }
+    lk.unlock();
+    uint64_t all_opened = 0;  // every rank mapped every peer, or everyone falls back
+    if ((rs = allreduce(&opened, &all_opened, 1, ROp::Min, st))) return rs;
+    if (!all_opened) {
+      set_detail("peer buffers not mappable (CUDA IPC); send/recv exchange used");
+      return RADSORT_ERR_UNSUPPORTED;
+    }
+    return RADSORT_OK;
+  }
 };
 
 // In-process loopback group: G host threads act as ranks on one device.
@@ -183,7 +276,8 @@ struct LoopGroup {
   std::vector<std::vector<uint64_t>> slot;
   std::vector<const uint8_t*> sbase;
   std::vector<std::vector<Msg>> sends;
-  explicit LoopGroup(int g) : G(g), slot(g), sbase(g), sends(g) {}
+  std::vector<uint8_t*> rbase;
+  explicit LoopGroup(int g) : G(g), slot(g), sbase(g), sends(g), rbase(g) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const uint64_t my = gen;
@@ -256,6 +350,14 @@ struct LoopTransport : Transport {
     grp->barrier();
     return rs;
   }
+  // every rank's buffer lives on this device in this process
+  radsort_status peer_bases(uint8_t* mine, std::vector<uint8_t*>& out, Context*, cudaStream_t) override {
+    grp->rbase[r] = mine;
+    grp->barrier();
+    out = grp->rbase;
+    grp->barrier();
+    return RADSORT_OK;
+  }
 };
 
 // ------------------------------------------------------------- algorithm
@@ -263,6 +365,138 @@ static void set_digit(uint64_t* key, uint32_t K, uint32_t d, uint32_t v) {
   const uint32_t bi = K - 1 - d;
   const uint32_t w = bi >> 3, sh = 8 * (bi & 7);
   key[w] = (key[w] & ~(0xffull << sh)) | ((uint64_t)v << sh);
+}
+
+// Fused exchange + receive-side level (SURVEY.md §8(e) k_merge_scatter, §8(f)
+// NEXT-3).  After the level-0 pass and the boundary search, each rank's send
+// range to rank p is a run of d0 buckets in tmp ("pieces": the whole bucket,
+// or the part of a straddling bucket on p's side of the cut).  Instead of
+// sending the pieces and re-reading them on the receiver, every sender
+//   a. histograms its pieces by the next digit d0+1 (one local read),
+//   b. allgathers the piece histograms: every rank then knows, for every
+//      receiver r, the size of each (d0, d0+1) bin from every sender, hence
+//      where its own share of each bin lands in r's buffer (bins in (b, v)
+//      order, senders in rank order inside a bin),
+//   c. scatters its pieces by digit d0+1 straight into the receivers' record
+//      buffers (k_scatter<PEER>: the radix pass's coalesced run stores go over
+//      NVLink to the peer's HBM, so the transfer overlaps the pass tile by
+//      tile and no separate copy or receive-side pass over the data remains).
+// The receiver then sorts its (d0, d0+1) bins from digit d0+2 on: the whole
+// multi-GPU sort moves each record through HBM as often as the 1-GPU sort does.
+static radsort_status fused_exchange(Transport& tr, Context* ctx, const LayoutOps* ops, uint8_t* recs, uint8_t* tmp,
+                                     uint64_t n_local, const std::vector<uint64_t>& cut, const uint64_t* lbase,
+                                     const std::vector<uint64_t>& q, uint32_t d0, uint32_t R, uint32_t K,
+                                     const std::vector<uint8_t*>& peer, cudaStream_t st, radsort_stats& stats,
+                                     uint64_t* n_out) {
+  const int G = tr.size(), me = tr.rank();
+  radsort_status rs;
+  std::vector<uint32_t> poff, plen, pdst;  // piece = (destination rank, bucket)
+  std::vector<uint32_t> pbkt;
+  for (int p = 0; p < G; ++p)
+    for (int b = 0; b < 256; ++b) {
+      const uint64_t lo = std::max(cut[p], lbase[b]), hi = std::min(cut[p + 1], lbase[b + 1]);
+      if (hi > lo) {
+        poff.push_back((uint32_t)lo);
+        plen.push_back((uint32_t)(hi - lo));
+        pdst.push_back((uint32_t)p);
+        pbkt.push_back((uint32_t)b);
+      }
+    }
+  const uint32_t np = (uint32_t)poff.size();
+  PieceWs w;
+  std::vector<uint32_t> ph((size_t)np * 256);
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if ((rs = ops->piece_hist(ctx, w, tmp, poff.data(), plen.data(), np, d0 + 1, st, ph.data()))) return rs;
+  }
+  // dense table of this sender: cnt[(r * 256 + b) * 256 + v], u32 packed in u64 pairs
+  const size_t E = (size_t)G * 65536;
+  std::vector<uint32_t> tab(E, 0);
+  for (uint32_t i = 0; i < np; ++i)
+    for (int v = 0; v < 256; ++v) tab[((size_t)pdst[i] * 256 + pbkt[i]) * 256 + v] = ph[(size_t)i * 256 + v];
+  std::vector<uint32_t> all(E * (size_t)G);
+  if ((rs = tr.allgather(reinterpret_cast<const uint64_t*>(tab.data()), reinterpret_cast<uint64_t*>(all.data()),
+                         E / 2, st)))
+    return rs;
+  auto cnt = [&](int src, int r, size_t bv) { return all[(size_t)src * E + (size_t)r * 65536 + bv]; };
+  // offsets of the (b, v) bins in every receiver that one of my pieces goes to
+  std::vector<char> need(G, 0);
+  for (uint32_t i = 0; i < np; ++i) need[pdst[i]] = 1;
+  need[me] = 1;
+  std::vector<std::vector<uint64_t>> roff(G);
+  for (int r = 0; r < G; ++r) {
+    if (!need[r]) continue;
+    roff[r].resize(65537);
+    uint64_t run = 0;
+    for (size_t bv = 0; bv < 65536; ++bv) {
+      roff[r][bv] = run;
+      for (int p = 0; p < G; ++p) run += cnt(p, r, bv);
+    }
+    roff[r][65536] = run;
+    if (run != q[r]) {
+      set_detail("fused exchange: rank %d would receive %llu records, quota %llu", r, (unsigned long long)run,
+                 (unsigned long long)q[r]);
+      return RADSORT_ERR_CUDA;
+    }
+  }
+  std::vector<uint32_t> hbase((size_t)np * 256);
+  std::vector<uint64_t> hdst(np);
+  uint64_t sent = 0;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int r = (int)pdst[i];
+    for (int v = 0; v < 256; ++v) {
+      const size_t bv = (size_t)pbkt[i] * 256 + v;
+      uint64_t o = roff[r][bv];
+      for (int p = 0; p < me; ++p) o += cnt(p, r, bv);
+      hbase[(size_t)i * 256 + v] = (uint32_t)o;
+    }
+    hdst[i] = (uint64_t)(uintptr_t)peer[r];
+    if (r != me) sent += plen[i];
+  }
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if ((rs = ops->piece_scatter(ctx, w, tmp, hbase.data(), hdst.data(), st))) return rs;
+  }
+  if ((rs = tr.barrier(st))) return rs;  // every sender's stores into this rank's buffer are complete
+  // receive side: the (d0, d0+1) bins, sorted from digit d0+2 on
+  std::vector<uint32_t> seg_off, seg_len;
+  uint64_t recv_other = 0;
+  for (size_t bv = 0; bv < 65536; ++bv) {
+    const uint64_t len = roff[me][bv + 1] - roff[me][bv];
+    if (len) {
+      seg_off.push_back((uint32_t)roff[me][bv]);
+      seg_len.push_back((uint32_t)len);
+    }
+    recv_other += len - cnt(me, me, bv);
+  }
+  const uint64_t got = roff[me][65536];
+  stats.nvlink_bytes_sent = sent * R;
+  stats.nvlink_bytes_recv = recv_other * R;
+  radsort_stats sub = {};
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if ((rs = ops->sort_segs(ctx, recs, tmp, (uint32_t)got, seg_off.data(), seg_len.data(), (uint32_t)seg_off.size(),
+                             d0 + 2, st, sub)))
+      return rs;
+  }
+  stats.levels = sub.levels;
+  stats.scatter_passes = sub.scatter_passes + 2;
+  stats.records_scattered = sub.records_scattered + 2 * n_local;
+  stats.records_hist = sub.records_hist + 2 * n_local;
+  stats.records_local = sub.records_local;
+  stats.records_tiny = sub.records_tiny;
+  for (int k = 0; k < RADSORT_K_COUNT; ++k) {
+    stats.kernel_launches[k] += sub.kernel_launches[k];
+    stats.kernel_ms[k] += sub.kernel_ms[k];
+    stats.kernel_bytes[k] += sub.kernel_bytes[k];
+  }
+  stats.kernel_launches[RADSORT_K_HIST] += 2;
+  stats.kernel_launches[RADSORT_K_SCATTER] += 1;
+  stats.kernel_launches[RADSORT_K_PLAN] += 2;
+  stats.exchange = 2;
+  stats.n = got;
+  *n_out = got;
+  return RADSORT_OK;
 }
 
 static radsort_status sort_multi_impl(Transport& tr, uint8_t* recs, uint8_t* tmp, uint64_t n_local, uint64_t capacity,
@@ -445,6 +679,23 @@ static radsort_status sort_multi_impl(Transport& tr, uint8_t* recs, uint8_t* tmp
   }
   for (int g = 1; g <= G; ++g) cut[g] = std::max(cut[g], cut[g - 1]);
 
+  // 6'. fused exchange (the product path when every rank can map its peers'
+  // record buffers: NVLink P2P through CUDA IPC, or one device for the
+  // loopback ranks).  Otherwise the send/recv exchange below.
+  {
+    const char* fe = getenv("RADSORT_MULTI_FUSED");
+    const bool want = !(fe && fe[0] == '0') && d0 + 1 < K && ops->piece_hist && ops->piece_scatter;
+    uint64_t want_all = 0, mine_w = want ? 1 : 0;
+    if ((rs = tr.allreduce(&mine_w, &want_all, 1, ROp::Min, st))) return rs;
+    if (want_all) {
+      std::vector<uint8_t*> peer;
+      rs = tr.peer_bases(recs, peer, ctx, st);
+      if (rs == RADSORT_OK)
+        return fused_exchange(tr, ctx, ops, recs, tmp, n_local, cut, lbase, q, d0, R, K, peer, st, stats, n_out);
+      if (rs != RADSORT_ERR_UNSUPPORTED) return rs;
+    }
+  }
+
   // 6. exchange.  Each destination's records are contiguous in tmp and grouped
   // by their top digit d0 (step 3); they go out as one message per bucket so
   // that every receiver lands its records bucket by bucket (bucket b from all
@@ -486,6 +737,7 @@ static radsort_status sort_multi_impl(Transport& tr, uint8_t* recs, uint8_t* tmp
     return RADSORT_ERR_CUDA;
   }
   if ((rs = tr.exchange(tmp, sends, recs, recvs, st))) return rs;
+  stats.exchange = 1;
   stats.nvlink_bytes_sent = (n_local - sc[me]) * R;
   stats.nvlink_bytes_recv = (got - S[(size_t)me * G + me]) * R;
 

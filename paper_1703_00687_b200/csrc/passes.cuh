@@ -570,7 +570,7 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
 constexpr int SCATTER_PAD = 64;  // dynamic smem beyond the TB-byte tile: the pad slot of absent records
 
-template <int R, int K, int TB, int SB, int MINB, bool PRE>
+template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
                                                        const uint32_t* __restrict__ carry_in, uint32_t hist_grid,
                                                        uint32_t* __restrict__ splitc,
                                                        const unsigned long long* __restrict__ probes,
-                                                       const uint32_t* __restrict__ tile_seg) {
+                                                       const uint32_t* __restrict__ tile_seg,
+                                                       const unsigned long long* __restrict__ seg_dst = nullptr) {
   constexpr uint32_t T = tile_recs<R, TB, SB>();
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
@@ -631,7 +632,11 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     const uint32_t lt = t - tile_start[s];
     const uint32_t base = sg.off + lt * T;
     const uint32_t m = min(T, sg.len - lt * T);
-    uint8_t* dst = buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
+    // PEER (multi-GPU fused exchange): segment s is written into the buffer at
+    // seg_dst[s] -- another GPU's records, mapped over NVLink -- and segbase
+    // holds record offsets in that buffer
+    uint8_t* dst = PEER ? reinterpret_cast<uint8_t*>(__ldg(seg_dst + s))
+                        : buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
     if (sg.mode == MODE_SCATTER) {
       const uint32_t d = sg.depth;
       uint32_t pre_excl = 0;
@@ -778,6 +783,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     __syncthreads();  // stage / gofs / sh_* reuse
     RS_PROF(5);
   }
+  if constexpr (PEER) __threadfence_system();  // peer stores performed before the kernel's completion is observed
   if (tid == 0 && moved) atomicAdd(&ctl->rec_scatter, moved);
 #ifdef RADSORT_PHASE_PROF
   if (tid == 0) {

@@ -40,7 +40,8 @@ Context* get_or_create_ctx(int dev) {
 const LayoutOps* layout_ops(uint32_t R, uint32_t K) {
 #define RS_OPS(r, k) \
   static const LayoutOps ops_##r##_##k = {run_layout<r, k>, run_layout_segs<r, k>, multi_hist<r, k>, \
-                                          multi_scatter<r, k>, multi_bounds<r, k>}
+                                          multi_scatter<r, k>, multi_bounds<r, k>, multi_piece_hist<r, k>, \
+                                          multi_piece_scatter<r, k>}
   RS_OPS(8, 8);
   RS_OPS(16, 8);
   RS_OPS(16, 16);
@@ -270,6 +271,7 @@ void radsort_finalize(void) {
                       &c->probes,   &c->tile_seg, &c->tile_pre};
     for (auto* b : bufs)
       if (b->p) cudaFree(b->p);
+    for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     for (auto& ev : c->ev)
       if (ev) cudaEventDestroy(ev);

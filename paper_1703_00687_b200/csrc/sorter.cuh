@@ -291,9 +291,11 @@ struct Sorter {
   // lookback: the decoupled look-back status words (tiles x 256 u64) are
   // needed (RADSORT_LOOKBACK=1, multi-GPU level-0 pass); otherwise the
   // reduce-then-scan tile prefixes (tiles x 256 u32).
-  static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v, bool lookback = false) {
-    const size_t capL = (size_t)n / C + 4;
-    const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4;
+  // extra: initial segments of a presegmented input (multi-GPU receive side), any size
+  static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v, bool lookback = false,
+                                uint32_t extra = 0) {
+    const size_t capL = (size_t)n / C + 4 + extra;
+    const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4 + extra;
     const size_t tiles_max = (size_t)n / T + capL + 4;
     radsort_status rs;
     if ((rs = ensure(ctx->large[0], capL * sizeof(Seg)))) return rs;
@@ -366,7 +368,7 @@ struct Sorter {
     smem_attr(ctx, k_scatter<R, K, TB, SB, MINB, true>, TB + SCATTER_PAD);
     const bool pre = !(getenv("RADSORT_LOOKBACK") && getenv("RADSORT_LOOKBACK")[0] == '1');
     Views v;
-    radsort_status rs = prepare(ctx, n, T, v, !pre);
+    radsort_status rs = prepare(ctx, n, T, v, !pre, init ? init->nseg : 0u);
     if (rs) return rs;
     Seg** L = v.L;
     Seg** Lo = v.Lo;
@@ -654,6 +656,84 @@ radsort_status multi_scatter(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t
   RS_CUDA(cudaGetLastError());
   RS_CUDA(cudaStreamSynchronize(st));
   workspace_release(ctx, st);
+  return RADSORT_OK;
+}
+
+// Fused exchange (multi-GPU, SURVEY.md §8(e) k_merge_scatter + §8(f) NEXT-3):
+// the sender's level-0 buckets, cut into pieces by destination rank, are
+// histogrammed by the next digit (multi_piece_hist) and then scattered by that
+// digit straight into the destination ranks' record buffers (multi_piece_scatter,
+// k_scatter<PEER>: remote stores over NVLink), at offsets the host derives
+// from every rank's piece histograms.  The per-call workspace keeps the
+// reduce-then-scan tile prefixes between the two calls, so other users of the
+// context (loopback ranks sharing the device) cannot clobber them.
+constexpr int PIECE_TB = 32768, PIECE_SB = 256, PIECE_MINB = 4;
+
+template <int R, int K>
+radsort_status multi_piece_hist(Context* ctx, PieceWs& w, const uint8_t* src, const uint32_t* off,
+                                const uint32_t* len, uint32_t np, uint32_t digit, cudaStream_t st, uint32_t* h_hist) {
+  constexpr uint32_t T = tile_recs<R, PIECE_TB, PIECE_SB>();
+  w.np = np;
+  if (np == 0) return RADSORT_OK;
+  size_t tiles = 0;
+  std::vector<Seg> segs(np);
+  for (uint32_t i = 0; i < np; ++i) {
+    segs[i] = {off[i], len[i], (uint8_t)digit, SRC_TMP, MODE_SCATTER, 0, 0};
+    tiles += (len[i] + T - 1) / T;
+  }
+  w.hist_grid = (uint32_t)ctx->sms * 4;
+  w.tiles = tiles;
+  radsort_status rs;
+  if ((rs = ensure(w.segs, np * sizeof(Seg))) || (rs = ensure(w.tile_start, (np + 1) * 4)) ||
+      (rs = ensure(w.tile_seg, (tiles + 1) * 4)) || (rs = ensure(w.hist, (size_t)np * RADIX * 4)) ||
+      (rs = ensure(w.andor, (size_t)np * 8 * 8)) || (rs = ensure(w.tile_pre, (tiles + 1) * RADIX * 4)) ||
+      (rs = ensure(w.ch_first, w.hist_grid * 4)) || (rs = ensure(w.ch_last, w.hist_grid * 4)) ||
+      (rs = ensure(w.ch_tot, (size_t)w.hist_grid * RADIX * 4)) ||
+      (rs = ensure(w.carry_in, (size_t)w.hist_grid * RADIX * 4)) || (rs = ensure(w.ctl, sizeof(Ctl))) ||
+      (rs = ensure(w.segbase, (size_t)np * RADIX * 4)) || (rs = ensure(w.dst, (size_t)np * 8)))
+    return rs;
+  Seg* dsegs = (Seg*)w.segs.p;
+  Ctl* ctl = (Ctl*)w.ctl.p;
+  RS_CUDA(cudaMemcpyAsync(dsegs, segs.data(), np * sizeof(Seg), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+  RS_CUDA(cudaMemsetAsync(w.hist.p, 0, (size_t)np * RADIX * 4, st));
+  RS_CUDA(cudaMemsetAsync(w.andor.p, 0, (size_t)np * 8 * 8, st));
+  k_prep<<<1, 1024, 0, st>>>(dsegs, np, T, (uint32_t*)w.tile_start.p, ctl, 1);
+  k_tilemap<<<(unsigned)std::max<size_t>(1, std::min<size_t>((tiles + 255) / 256, (size_t)ctx->sms * 16)), 256, 0, st>>>(
+      (const uint32_t*)w.tile_start.p, np, ctl, (uint32_t*)w.tile_seg.p);
+  k_hist_pre<R, K, T><<<w.hist_grid, HIST_B, 0, st>>>(
+      dsegs, (const uint32_t*)w.tile_start.p, np, ctl, (uint32_t*)w.hist.p, (unsigned long long*)w.andor.p, src, src,
+      (uint32_t*)w.tile_pre.p, (uint32_t*)w.ch_first.p, (uint32_t*)w.ch_last.p, (uint32_t*)w.ch_tot.p,
+      (const uint32_t*)w.tile_seg.p);
+  k_carry<<<1, RADIX, 0, st>>>((const uint32_t*)w.ch_first.p, (const uint32_t*)w.ch_last.p,
+                               (const uint32_t*)w.ch_tot.p, w.hist_grid, (uint32_t*)w.carry_in.p);
+  RS_CUDA(cudaGetLastError());
+  RS_CUDA(cudaMemcpyAsync(h_hist, w.hist.p, (size_t)np * RADIX * 4, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  return RADSORT_OK;
+}
+
+// h_base[i * 256 + v]: record offset, in the buffer at h_dst[i], of the first
+// record of piece i with digit v (this sender's share of that bin).
+template <int R, int K>
+radsort_status multi_piece_scatter(Context* ctx, PieceWs& w, const uint8_t* src, const uint32_t* h_base,
+                                   const uint64_t* h_dst, cudaStream_t st) {
+  const uint32_t np = w.np;
+  if (np == 0) return RADSORT_OK;
+  auto* kfn = k_scatter<R, K, PIECE_TB, PIECE_SB, PIECE_MINB, true, true>;
+  smem_attr(ctx, kfn, PIECE_TB + SCATTER_PAD);
+  RS_CUDA(cudaMemcpyAsync(w.segbase.p, h_base, (size_t)np * RADIX * 4, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(w.dst.p, h_dst, (size_t)np * 8, cudaMemcpyHostToDevice, st));
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, PIECE_SB, PIECE_TB + SCATTER_PAD);
+  const unsigned gs = (unsigned)std::max<size_t>(1, std::min(w.tiles, (size_t)ctx->sms * std::max(occ, 1)));
+  kfn<<<gs, PIECE_SB, PIECE_TB + SCATTER_PAD, st>>>(
+      (const Seg*)w.segs.p, (const uint32_t*)w.tile_start.p, np, (const uint32_t*)w.segbase.p, nullptr, 0,
+      (Ctl*)w.ctl.p, const_cast<uint8_t*>(src), const_cast<uint8_t*>(src), (const uint32_t*)w.tile_pre.p,
+      (const uint32_t*)w.ch_first.p, (const uint32_t*)w.carry_in.p, w.hist_grid, nullptr, nullptr,
+      (const uint32_t*)w.tile_seg.p, (const unsigned long long*)w.dst.p);
+  RS_CUDA(cudaGetLastError());
+  RS_CUDA(cudaStreamSynchronize(st));
   return RADSORT_OK;
 }
 

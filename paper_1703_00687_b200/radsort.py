@@ -39,6 +39,7 @@ class Stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_uint32 * 7), ("kernel_ms", ctypes.c_float * 7),
         ("kernel_bytes", ctypes.c_uint64 * 7),
         ("bins_split", ctypes.c_uint64), ("records_split", ctypes.c_uint64),
+        ("exchange", ctypes.c_uint32), ("reserved_", ctypes.c_uint32),
     ]
 
 

@@ -20,7 +20,7 @@ import oracle  # noqa: E402
 from datagen import host as dg  # noqa: E402
 
 
-def run_loopback(shards, K, slack=1024):
+def run_loopback(shards, K, slack=1024, stats=None):
     import paper_1703_00687_b200 as rs
 
     G = len(shards)
@@ -43,6 +43,8 @@ def run_loopback(shards, K, slack=1024):
             st = torch.cuda.Stream()
             outs[g] = grp.sort(g, recs[g], tmps[g], shards[g].shape[0], K, stream=st)
             st.synchronize()
+            if stats is not None:
+                stats[g] = rs.last_stats()  # thread-local: this rank's call
         except Exception as e:  # noqa: BLE001
             errs[g] = e
 
@@ -71,7 +73,11 @@ def _init():
 @pytest.mark.parametrize("R,K,dist", [(8, 8, "uniform"), (16, 8, "uniform40"), (8, 8, "zipf"), (32, 16, "uniform"),
                                       (16, 16, "bytes"), (8, 8, "few"), (16, 8, "equal"), (24, 8, "uniform"),
                                       (40, 16, "zipf")])
-def test_loopback_multi(G, R, K, dist):
+@pytest.mark.parametrize("fused", [1, 0])
+def test_loopback_multi(G, R, K, dist, fused, monkeypatch):
+    # fused = 1: the product path (next-digit scatter straight into the peers'
+    # buffers); 0: the send/recv exchange
+    monkeypatch.setenv("RADSORT_MULTI_FUSED", str(fused))
     rng = np.random.default_rng(G * 100 + R)
     sizes = [int(x) for x in rng.integers(20_000, 120_000, G)]
     if G >= 3:
@@ -79,10 +85,12 @@ def test_loopback_multi(G, R, K, dist):
     first = np.concatenate([[0], np.cumsum(sizes)])
     payload = "index" if R > K else "random"
     shards = [dg.generate(sizes[g], R, K, dist, payload=payload, seed=31, first=int(first[g])) for g in range(G)]
-    out = run_loopback(shards, K)
+    st = [None] * G
+    out = run_loopback(shards, K, stats=st)
     got = np.concatenate(out)
     a = np.concatenate(shards)
     assert oracle.compare(got, oracle.sort(a, K), K) == -1
+    assert all(s["exchange"] == (2 if fused else 1) for s in st), [s["exchange"] for s in st]
 
 
 def test_loopback_heavy_key_straddles_boundaries():
@@ -94,8 +102,13 @@ def test_loopback_heavy_key_straddles_boundaries():
     w[1::5, 0] = 12345
     w[2::5, 0] = 12345
     shards = np.array_split(a, G)
-    out = run_loopback([np.ascontiguousarray(s) for s in shards], K)
-    assert oracle.compare(np.concatenate(out), oracle.sort(a, K), K) == -1
+    for fused in ("1", "0"):
+        os.environ["RADSORT_MULTI_FUSED"] = fused
+        try:
+            out = run_loopback([np.ascontiguousarray(s) for s in shards], K)
+        finally:
+            os.environ.pop("RADSORT_MULTI_FUSED", None)
+        assert oracle.compare(np.concatenate(out), oracle.sort(a, K), K) == -1
 
 
 def test_nccl_single_rank():
@@ -117,6 +130,7 @@ def test_nccl_single_rank():
         n_out = rs.sort_multi(rec, tmp, a.shape[0], 8)
         torch.cuda.synchronize()
         assert n_out == a.shape[0]
+        assert rs.last_stats()["exchange"] == 2  # fused exchange: the buffer is exported by CUDA IPC
         assert oracle.compare(rec.cpu().numpy(), oracle.sort(a, 8), 8) == -1
     finally:
         if created:
