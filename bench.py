@@ -351,6 +351,30 @@ def run_radsort(args):
 
     # end to end through the public C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
+    if world > 1 and not args.no_e2e:
+        # every rank: H2D of its pinned input shard, the collective sort, D2H of its output shard;
+        # the step time is the max over ranks
+        host_in = pristine.cpu().pin_memory()
+        e2e_t, out_bytes = [], 0
+        for i in range(args.e2e_steps + 1):
+            host_out = torch.empty((cap, R), dtype=torch.uint8).pin_memory()
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            rec[:n].copy_(host_in, non_blocking=True)
+            n_out = rs.sort_multi(rec, tmp, n, K)
+            host_out[:n_out].copy_(rec[:n_out], non_blocking=True)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if i > 0:
+                e2e_t.append(float(t.item()))
+            out_bytes = n_out * R
+        e2e = {"value": round(N_total / statistics.median(e2e_t) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": n * R, "d2h_bytes_per_step": out_bytes,
+               "note": "per rank; max over ranks of the wall time"}
+        del host_in, host_out
     if world == 1 and not args.no_e2e:
         host_pristine = pristine.cpu().pin_memory()
         host = torch.empty_like(host_pristine).pin_memory()
@@ -392,6 +416,11 @@ def run_radsort(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if world > 1:
+            line["multi"] = {"exchange": {2: "fused (next-digit scatter into the peers' buffers over NVLink)",
+                                          1: "NCCL send/recv"}.get(stats.get("exchange", 0), "none"),
+                             "nvlink_bytes_sent_rank0": stats["nvlink_bytes_sent"],
+                             "nvlink_bytes_recv_rank0": stats["nvlink_bytes_recv"]}
         if kmc:  # the step also run-length counts the sorted k-mers (inside the timed region)
             line["kmc"] = {"unique_keys": uc["unique"], "unique_count_ms_per_step": round(uc["ms"] / args.steps, 4),
                            "note": "value/ms_per_step include the unique-count kernels; e2e is the sort alone"}

@@ -55,7 +55,9 @@ enum {
   RADSORT_K_CHILDREN = 4,/* classify child bins; sort tiny ones; copy final ones        */
   RADSORT_K_LOCAL = 5,  /* CTA-local shared-memory sort of a bin <= C records           */
   RADSORT_K_MULTI = 6,  /* multi-GPU exchange-side kernels                               */
-  RADSORT_K_COUNT = 7
+  RADSORT_K_GATHER = 7, /* key + index sort: build the (key, index) records, gather the
+                           full records in sorted order (wide records, NEXT-1)          */
+  RADSORT_K_COUNT = 8
 };
 
 typedef struct {
@@ -79,7 +81,7 @@ typedef struct {
   uint64_t records_split;     /* records of those dominant keys (final after the split) */
   uint32_t exchange;          /* multi-GPU: 1 = send/recv exchange, 2 = fused exchange
                                  (next-digit scatter straight into the peers' buffers) */
-  uint32_t reserved_;
+  uint32_t key_index;         /* 1: sorted as (key, index) records + one payload gather */
 } radsort_stats;
 
 /* Create the per-(process, device) context for `device` (cudaSetDevice is the

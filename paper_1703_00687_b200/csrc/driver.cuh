@@ -57,6 +57,7 @@ struct Context {
   bool done_valid = false;
   DevBuf mprobe, mlo, mhi, mlt, mle;  // multi-GPU splitter search scratch
   std::map<std::string, void*> ipc_open;  // peer buffers opened by CUDA IPC (handle bytes -> mapped base)
+  DevBuf kiw;                             // key + index sort: the (key, index) records and their scratch
 };
 
 // Order `st` after the previous user of the workspace (another stream may still

@@ -2,6 +2,8 @@
 // rec_size=32, key_size=8.
 #include "sorter.cuh"
 namespace radsort {
+// the (key, index) records of the key + index sort are sorted by layout_16_8.cu's instantiation
+extern template radsort_status run_layout<16, 8>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
 template radsort_status run_layout_segs<32, 8>(Context*, uint8_t*, uint8_t*, uint32_t, const uint32_t*,
                                                   const uint32_t*, uint32_t, uint32_t, cudaStream_t, radsort_stats&);
 template radsort_status run_layout<32, 8>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);

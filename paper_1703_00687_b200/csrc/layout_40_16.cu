@@ -2,6 +2,8 @@
 // rec_size=40, key_size=16.
 #include "sorter.cuh"
 namespace radsort {
+// the (key, index) records of the key + index sort are sorted by layout_24_16.cu's instantiation
+extern template radsort_status run_layout<24, 16>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);
 template radsort_status run_layout_segs<40, 16>(Context*, uint8_t*, uint8_t*, uint32_t, const uint32_t*,
                                                   const uint32_t*, uint32_t, uint32_t, cudaStream_t, radsort_stats&);
 template radsort_status run_layout<40, 16>(Context*, uint8_t*, uint8_t*, uint32_t, cudaStream_t, radsort_stats&);

@@ -268,7 +268,7 @@ void radsort_finalize(void) {
     DevBuf* bufs[] = {&c->large[0], &c->large[1], &c->local[0], &c->local[1], &c->hist,     &c->andor,
                       &c->segbase,  &c->tile_start, &c->status, &c->ctl,   &c->host_io[0], &c->host_io[1],
                       &c->mprobe,   &c->mlo,      &c->mhi,      &c->mlt,   &c->mle,       &c->splitc,
-                      &c->probes,   &c->tile_seg, &c->tile_pre};
+                      &c->probes,   &c->tile_seg, &c->tile_pre, &c->kiw};
     for (auto* b : bufs)
       if (b->p) cudaFree(b->p);
     for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);

@@ -98,16 +98,29 @@ struct Sorter {
     }
   }
 
-  // ---- cluster-local sort (bins of C < n <= CCAP records, k_local_cluster)
-  static constexpr int CS = 4;
-  static constexpr uint32_t LCS = 2;
+  // ---- cluster-local sort (bins of CL_MIN <= n <= ccap() records, k_local_cluster)
+  // One shape: clusters of 4 CTAs of 512 threads, one per SM (132 SMs: a GPC
+  // holds no fifth 4-CTA cluster).  Measured and dropped: 8 CTAs of 256 threads,
+  // two per SM (c4 local 32.5 -> 42.5 ms: the same 33 bins in flight -- the
+  // register file holds one bin per 4 SMs either way -- with 7/8 instead of
+  // 3/4 of the records crossing DSMEM).
   static constexpr uint32_t CL_W = R >= 24 ? 14 : 15;                     // composite digit width cap
-  static constexpr size_t CL_CNT = (size_t)2 << CL_W;                      // 2^W u16 counters / bases
-  static constexpr size_t CL_SST = CL_CNT >> LCS;                          // the slice's bucket starts
-  static constexpr uint32_t CL_STAGE_CAP = (uint32_t)((LOCAL_SMEM_MAX - CL_CNT - CL_SST - 2048) / (R + 2));
-  static constexpr int CL_ILMAX = R <= 8 ? 32 : (R <= 16 ? 16 : 8);  // register budget of the record array
-  static constexpr uint32_t CCAP_SMEM = CL_STAGE_CAP / 5 * 4 * CS;       // 20 % slack for uneven bucket slices
-  static constexpr uint32_t CCAP = CCAP_SMEM < (uint32_t)(CL_ILMAX * 512 * CS) ? CCAP_SMEM : CL_ILMAX * 512 * CS;
+  static constexpr int CL_ILMAX = R <= 8 ? 32 : (R <= 16 ? 16 : 8);       // register budget of the record array
+  template <int CS_, int LB_, int MINB_>
+  struct ClCfg {
+    static constexpr int CS = CS_, LB = LB_, MINB = MINB_;
+    static constexpr uint32_t LCS = CS == 2 ? 1u : (CS == 4 ? 2u : 3u);
+    static constexpr size_t CNT = (size_t)2 << CL_W;                       // 2^W u16 counters / bases
+    static constexpr size_t SST = CNT >> LCS;                               // the slice's bucket starts
+    static constexpr size_t SMEM = MINB == 1 ? LOCAL_SMEM_MAX : (size_t)228 * 1024 / MINB - 1536;
+    // smem: stage | counters | slice starts | collision list
+    static constexpr uint32_t STAGE_CAP = (uint32_t)((SMEM - CNT - SST - 2048) / (R + 2));
+    // 20 % slack for uneven bucket slices (an overflowing slice hands the bin back to the Large list)
+    static constexpr uint32_t CCAP_SMEM = STAGE_CAP / 5 * 4 * CS;
+    static constexpr uint32_t CCAP = CCAP_SMEM < (uint32_t)(CL_ILMAX * LB * CS) ? CCAP_SMEM : CL_ILMAX * LB * CS;
+  };
+  using Cl4 = ClCfg<4, 512, 1>;
+  static uint32_t ccap() { return Cl4::CCAP; }
   // smaller bins (C < n < CL_MIN) take a further radix level: below ~2.5 C the
   // cluster's per-bin phases cost more than the pass they save (measured, R = 32)
   static constexpr uint32_t CL_MIN = C * 5 / 2;
@@ -123,40 +136,47 @@ struct Sorter {
     return R >= 24 && e && e[0] == '1';
   }
 
-  template <int IL, bool DW>
+  template <int IL, bool DW, class CF>
   static void launch_cluster_t(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
                                Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
     const int sms = ctx->sms;
     const uint32_t wmax = CL_W;
-    const size_t stage_bytes = DW ? 0 : ((size_t)CL_STAGE_CAP * R + 15) & ~(size_t)15;
-    const uint32_t cap = DW ? CCAP / 2 + 1 : CL_STAGE_CAP / 2 + 1;
-    const size_t smem = stage_bytes + CL_CNT + CL_SST + (((size_t)cap * 4 + 15) & ~(size_t)15);
-    auto* kfn = k_local_cluster<R, K, IL, 512, CS, DW>;
-    smem_attr(ctx, kfn, (int)LOCAL_SMEM_MAX);
+    const size_t stage_bytes = DW ? 0 : ((size_t)CF::STAGE_CAP * R + 15) & ~(size_t)15;
+    const uint32_t cap = DW ? CF::CCAP / 2 + 1 : CF::STAGE_CAP / 2 + 1;
+    const size_t smem = stage_bytes + CF::CNT + CF::SST + (((size_t)cap * 4 + 15) & ~(size_t)15);
+    auto* kfn = k_local_cluster<R, K, IL, CF::LB, CF::CS, DW>;
+    smem_attr(ctx, kfn, (int)CF::SMEM);
     int& max_clusters = ctx->max_clusters[(const void*)kfn];  // per device (the context's)
     if (!max_clusters) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(CS * sms / CS, 1, 1);
-      cfg.blockDim = dim3(512, 1, 1);
-      cfg.dynamicSmemBytes = LOCAL_SMEM_MAX;
-      if (cudaOccupancyMaxActiveClusters(&max_clusters, kfn, &cfg) != cudaSuccess ||
-          max_clusters <= 0) {
+      cfg.gridDim = dim3(CF::CS * sms, 1, 1);
+      cfg.blockDim = dim3(CF::LB, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kfn, &cfg) != cudaSuccess || max_clusters <= 0) {
         cudaGetLastError();
-        max_clusters = sms / CS;
+        max_clusters = sms * CF::MINB / CF::CS;
       }
+      if (getenv("RADSORT_LOG"))
+        fprintf(stderr, "[radsort] k_local_cluster %dx%d: %d clusters resident, %zu B smem per CTA\n", CF::CS, CF::LB,
+                max_clusters, smem);
     }
     const unsigned clusters = (unsigned)std::max<size_t>(1, std::min<size_t>(nloc, (size_t)max_clusters));
-    kfn<<<clusters * CS, 512, smem, st>>>(
-        list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)CL_CNT, cap, next, nxt, large_next, ctl, recs, tmp);
+    kfn<<<clusters * CF::CS, CF::LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)CF::CNT, cap, next,
+                                                  nxt, large_next, ctl, recs, tmp);
   }
 
-  static void launch_cluster(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
-                             Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
-    const uint32_t il = (maxlen + CS * 512 - 1) / (CS * 512);  // records per thread
-#define RS_CL(IL)                                                                                       \
-  do {                                                                                                  \
-    if (cluster_dw()) launch_cluster_t<IL, true>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st); \
-    else launch_cluster_t<IL, false>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st); \
+  template <class CF>
+  static void launch_cluster_c(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
+                               Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
+    const uint32_t il = (maxlen + CF::CS * CF::LB - 1) / (CF::CS * CF::LB);  // records per thread
+#define RS_CL(IL)                                                                                                  \
+  do {                                                                                                             \
+    bool dw_ = false;                                                                                              \
+    if constexpr (CF::CS == 4) {                                                                                   \
+      if ((dw_ = cluster_dw()))                                                                                    \
+        launch_cluster_t<IL, true, CF>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st);        \
+    }                                                                                                              \
+    if (!dw_) launch_cluster_t<IL, false, CF>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st); \
   } while (0)
     if (il <= 2) RS_CL(2);
     else if (il <= 4) RS_CL(4);
@@ -172,6 +192,10 @@ struct Sorter {
       RS_CL(8);
     }
 #undef RS_CL
+  }
+  static void launch_cluster(Context* ctx, uint32_t nloc, uint32_t maxlen, const Seg* list, Seg* next, int nxt,
+                             Seg* large_next, Ctl* ctl, uint8_t* recs, uint8_t* tmp, cudaStream_t st) {
+    launch_cluster_c<Cl4>(ctx, nloc, maxlen, list, next, nxt, large_next, ctl, recs, tmp, st);
   }
 
   static void set_attrs(Context* ctx) { smem_attr(ctx, k_children<R, K>, CHILD_SCRATCH); }
@@ -380,7 +404,7 @@ struct Sorter {
     Ctl* ctl = v.ctl;
     const size_t tiles_max = v.tiles_max;
 
-    // cluster-local sorting of bins of CL_MIN..CCAP records: on for R = 32, the
+    // cluster-local sorting of bins of CL_MIN..ccap() records: on for R = 32, the
     // one layout where it beats a further radix level (measured);
     // RADSORT_CLUSTER=1 forces it on for every layout, =0 off
     const char* cl_env = getenv("RADSORT_CLUSTER");
@@ -491,7 +515,7 @@ struct Sorter {
         tm.begin(RADSORT_K_CHILDREN);
         k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
                                                                   tmp, v.probes, local_max() > C ? C + 1 : CL_MIN,
-                                                                  local_max() > C ? local_max() : (cluster_ok ? CCAP : C),
+                                                                  local_max() > C ? local_max() : (cluster_ok ? ccap() : C),
                                                                   bitonic_max());
         tm.end();
         stats.kernel_launches[RADSORT_K_PLAN] += 2;
@@ -571,8 +595,121 @@ struct Sorter {
 };
 
 
+// ---------------------------------------------- NEXT-1: key + index sort
+// For records much wider than their key (PAPER.md:166-169
+// §3.3: with long records the record moves dominate, so move them once): sort
+// (key, 32-bit index) records of KI = 16 (K = 8) or 24 (K = 16) bytes with the
+// same MSD radix sort, then move every full record once, by a gather.
+//   k_ki_build : records -> a copy in tmp, and (key, i) into the workspace
+//   radix sort of the (key, index) records (layout (KI, K), tmp half as scratch)
+//   k_ki_gather: records[j] = copy[index of the j-th sorted pair]
+// The workspace holds 2 n KI bytes (the pairs and the radix sort's scratch).
+template <int R, int K, int KI>
+__global__ void __launch_bounds__(256) k_ki_build(const uint8_t* __restrict__ recs, uint8_t* __restrict__ copy,
+                                                  uint8_t* __restrict__ ki, uint32_t n) {
+  constexpr int U = 4;  // records in flight per thread
+  const uint32_t stride = gridDim.x * 256u * U;
+  for (uint32_t b = blockIdx.x * 256u * U; b < n; b += stride) {
+    Rec<R> r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = b + u * 256u + threadIdx.x;
+      if (i < n) r[u] = ldg_wide<R>(recs + (size_t)i * R);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = b + u * 256u + threadIdx.x;
+      if (i < n) {
+        stg_rec<R>(copy + (size_t)i * R, r[u]);
+        const Key<K> k = key_of<R, K>(r[u]);
+        uint8_t* q = ki + (size_t)i * KI;
+        if constexpr (KI == 16) {
+          *reinterpret_cast<uint4*>(q) = make_uint4((uint32_t)k.w0, (uint32_t)(k.w0 >> 32), i, 0u);
+        } else {
+          uint2* q2 = reinterpret_cast<uint2*>(q);
+          q2[0] = make_uint2((uint32_t)k.w0, (uint32_t)(k.w0 >> 32));
+          q2[1] = make_uint2((uint32_t)k.w1, (uint32_t)(k.w1 >> 32));
+          q2[2] = make_uint2(i, 0u);
+        }
+      }
+    }
+  }
+}
+
+template <int R, int K, int KI>
+__global__ void __launch_bounds__(256) k_ki_gather(const uint8_t* __restrict__ ki, const uint8_t* __restrict__ copy,
+                                                   uint8_t* __restrict__ recs, uint32_t n) {
+  constexpr int U = 8;  // independent random reads in flight per thread
+  const uint32_t stride = gridDim.x * 256u * U;
+  for (uint32_t b = blockIdx.x * 256u * U; b < n; b += stride) {
+    uint32_t src[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = b + u * 256u + threadIdx.x;
+      src[u] = j < n ? __ldg(reinterpret_cast<const uint32_t*>(ki + (size_t)j * KI + K)) : 0u;
+    }
+    Rec<R> r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = b + u * 256u + threadIdx.x;
+      if (j < n) r[u] = ldg_wide<R>(copy + (size_t)src[u] * R);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = b + u * 256u + threadIdx.x;
+      if (j < n) stg_rec<R>(recs + (size_t)j * R, r[u]);
+    }
+  }
+}
+
+template <int R, int K>
+struct KeyIndex {
+  static constexpr bool BUILT = (R == 32 && K == 8) || (R == 40 && K == 16);
+  static constexpr int KI = K == 8 ? 16 : 24;
+  // RADSORT_KEY_INDEX=1/0 forces it on/off; default: on where it was measured faster
+  static bool on() {
+    if constexpr (!BUILT) return false;
+    const char* e = getenv("RADSORT_KEY_INDEX");
+    return e ? e[0] == '1' : KI_DEFAULT;
+  }
+  // measured slower on B200 (profiles/r02_key_index_bench.jsonl: (32,8) 1 G 91.4 vs 67.0 ms,
+  // (40,16) 500 M 76.3 vs 69.5 ms -- the random 32/40-byte gather runs at a fraction of the
+  // sequential HBM rate): opt-in
+  static constexpr bool KI_DEFAULT = false;
+  static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
+                            radsort_stats& s) {
+    if constexpr (BUILT) {
+      radsort_status rs;
+      if ((rs = ensure(ctx->kiw, (size_t)2 * n * KI))) return rs;
+      uint8_t* ki = (uint8_t*)ctx->kiw.p;
+      const unsigned g = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)n + 1023) / 1024, (size_t)ctx->sms * 8));
+      Timer tm(ctx, st);
+      tm.begin(RADSORT_K_GATHER);
+      k_ki_build<R, K, KI><<<g, 256, 0, st>>>(recs, tmp, ki, n);
+      tm.end();
+      RS_CUDA(cudaGetLastError());
+      tm.flush(s);
+      if ((rs = run_layout<KI, K>(ctx, ki, ki + (size_t)n * KI, n, st, s))) return rs;
+      const unsigned gg = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)n + 2047) / 2048, (size_t)ctx->sms * 8));
+      tm.begin(RADSORT_K_GATHER);
+      k_ki_gather<R, K, KI><<<gg, 256, 0, st>>>(ki, tmp, recs, n);
+      tm.end();
+      RS_CUDA(cudaGetLastError());
+      tm.flush(s);
+      s.kernel_launches[RADSORT_K_GATHER] += 2;
+      s.kernel_bytes[RADSORT_K_GATHER] += (uint64_t)n * (2 * R + KI) + (uint64_t)n * (KI + 2 * R);
+      s.key_index = 1;
+      s.rec_size = R;
+    }
+    return RADSORT_OK;
+  }
+};
+
 template <int R, int K>
 radsort_status run_layout(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st, radsort_stats& s) {
+  if constexpr (KeyIndex<R, K>::BUILT) {
+    if (KeyIndex<R, K>::on() && n > Sorter<R, K>::C) return KeyIndex<R, K>::run(ctx, recs, tmp, n, st, s);
+  }
   workspace_acquire(ctx, st);
   const radsort_status rs = Sorter<R, K>::run(ctx, recs, tmp, n, st, s);
   workspace_release(ctx, st);

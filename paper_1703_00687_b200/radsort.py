@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RADSORT_LIB_PATH") or os.path.join(_HERE, "libradsort.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_NOT_INITIALIZED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_CAPACITY = range(8)
-KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "multi"]
+KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "multi", "gather"]
 
 # every symbol include/radsort.h declares
 EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
@@ -36,10 +36,10 @@ class Stats(ctypes.Structure):
         ("bins_large", ctypes.c_uint64), ("bins_local", ctypes.c_uint64), ("bins_tiny", ctypes.c_uint64),
         ("bins_final", ctypes.c_uint64),
         ("nvlink_bytes_sent", ctypes.c_uint64), ("nvlink_bytes_recv", ctypes.c_uint64),
-        ("kernel_launches", ctypes.c_uint32 * 7), ("kernel_ms", ctypes.c_float * 7),
-        ("kernel_bytes", ctypes.c_uint64 * 7),
+        ("kernel_launches", ctypes.c_uint32 * 8), ("kernel_ms", ctypes.c_float * 8),
+        ("kernel_bytes", ctypes.c_uint64 * 8),
         ("bins_split", ctypes.c_uint64), ("records_split", ctypes.c_uint64),
-        ("exchange", ctypes.c_uint32), ("reserved_", ctypes.c_uint32),
+        ("exchange", ctypes.c_uint32), ("key_index", ctypes.c_uint32),
     ]
 
 

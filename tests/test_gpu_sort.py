@@ -413,3 +413,20 @@ def test_opt_in_local_sorters(var, R, K, monkeypatch):
     for dist, n in (("uniform", 2_000_003), ("zipf", 1_500_001), ("few", 300_007), ("bytes", 700_001),
                     ("uniform40", 1_000_003)):
         check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=n % 97), K)
+
+
+@pytest.mark.parametrize("R,K", [(32, 8), (40, 16)])
+@pytest.mark.parametrize("ki", ["1", "0"])
+@pytest.mark.parametrize("dist", ["uniform", "zipf", "few", "equal", "bytes"])
+def test_key_index_sort(R, K, ki, dist, monkeypatch):
+    # NEXT-1: (key, index) records sorted by the radix sort, then one gather of
+    # the full records (RADSORT_KEY_INDEX=1), against the direct sort (=0);
+    # sizes below / at / above the CTA-local capacity and across several tiles
+    import paper_1703_00687_b200 as rs
+
+    monkeypatch.setenv("RADSORT_KEY_INDEX", ki)
+    for n in (C_of(R) - 1, C_of(R) + 1, 3 * T_of(R) + 17, 700_001):
+        a = dg.generate(n, R, K, dist, payload="random", seed=n + R)
+        check(a, K)
+        if n > C_of(R):
+            assert rs.last_stats()["key_index"] == (1 if ki == "1" else 0)

@@ -1,11 +1,7 @@
 #!/bin/bash
-# A/B of the cluster local sort variants on c4 + the tests that cover it.
+# the cluster local sort: tests that cover it + c4 timing (+ optional prof build run)
 set -u
-O=gpurun_out/r02
-mkdir -p $O
-timeout 600 python -m pytest tests -m gpu -x -q -k "cluster or multi or fuzz or c4 or level0 or outlier" > $O/pytest_cl.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_cl.log
-for dw in 0 1; do
-  RADSORT_CLUSTER_DW=$dw RADSORT_LOG=1 timeout 600 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/cl_dw$dw.json 2> $O/cl_dw$dw.err
-  echo "dw=$dw rc=$? $(grep 'level 1 ms' $O/cl_dw$dw.err | tail -1)"
-  python -c "import json;d=json.load(open('$O/cl_dw$dw.json'));print(d['ms_per_step'], d['kernel_ms_per_step'])"
-done
+O=gpurun_out/r02; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q -k "cluster or c4 or fuzz or multi or level0 or outlier" > $O/pytest_cl.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_cl.log | cut -c1-300
+RADSORT_LOG=1 timeout 600 python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/cl_c4.json 2> $O/cl_c4.err
+echo "c4 rc=$?"; python -c "import json;d=json.load(open('$O/cl_c4.json'));print(d['ms_per_step'], {k:round(v,2) for k,v in d['kernel_ms_per_step'].items() if v>0.05})"
