@@ -644,8 +644,16 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
         if (tid < RADIX) {
           const uint32_t per = (total + hist_grid - 1) / hist_grid;
           const uint32_t ch = t / per;
-          pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
-                     (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
+          if constexpr (R >= 24) {
+            // four independent loads (the carry is selected after they land, not loaded behind
+            // ch_first): c4 scatter 25.4 -> 24.0 ms; R <= 16 measured 1 % slower this way
+            const uint32_t cf = __ldg(ch_first + ch), ci = __ldg(carry_in + (size_t)ch * RADIX + tid);
+            pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
+                       (s == cf ? ci : 0u);
+          } else {
+            pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
+                       (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
+          }
         }
       }
       uint32_t rk[(I + 1) / 2];  // ranks < T <= 2^16: two per register (fewer live registers under the cap)
@@ -1066,14 +1074,31 @@ __device__ __forceinline__ bool local_finish(uint8_t* stage, const uint16_t* sta
     if (nbig) __syncthreads();
   }
   RS_FPROF(1);
-  if (bulk) {  // one TMA bulk store (out and n * R 16-byte aligned); the caller waits before reusing the stage
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out), "r"(sa), "r"(n * (uint32_t)R)
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  if (bulk) {
+    // one TMA bulk store of the 16-byte-aligned middle of the bin (stage and out
+    // agree mod 16: the caller shifts the stage); the head / tail words by threads;
+    // the caller waits for the bulk read before reusing the stage
+    const uintptr_t o0 = (uintptr_t)out, o1 = o0 + (size_t)n * R;
+    const uintptr_t a0 = (o0 + 15) & ~(uintptr_t)15, a1 = o1 & ~(uintptr_t)15;
+    if (a1 > a0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + (a0 - o0));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a0), "r"(sa),
+                     "r"((uint32_t)(a1 - a0))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      // 8-byte words outside [a0, a1): at most one before and one after
+      if (tid < 2) {
+        const uintptr_t w = tid == 0 ? o0 : a1;
+        if ((tid == 0 && a0 > o0) || (tid == 1 && o1 > a1))
+          *reinterpret_cast<uint2*>(w) = *reinterpret_cast<const uint2*>(stage + (w - o0));
+      }
+    } else {  // shorter than one aligned 16-byte chunk
+      for (uint32_t q = tid; q < n * (uint32_t)R / 8u; q += LB)
+        reinterpret_cast<uint2*>(out)[q] = reinterpret_cast<const uint2*>(stage)[q];
     }
   } else {
     for (uint32_t q = tid; q < n; q += LB) st_rec<R>(out + (size_t)q * R, ld_rec<R>(stage + (size_t)q * R));
@@ -1160,6 +1185,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
   if (tid == 0) { s_ncol = 0; s_nbig = 0; s_const = 0; }
   unsigned long long done = 0;
+  bool pending = false;  // the previous bin's bulk store may still read the stage
 #ifdef RADSORT_PHASE_PROF
   unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = clock64(), tB = 0;
 #define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
@@ -1174,6 +1200,13 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     const uint32_t n = sg.len;
     const int lim = (int)n - tid;
     uint8_t* out = recs + (size_t)sg.off * R;
+    // 512-thread CTAs (one bin per SM): the bin is staged at the same alignment
+    // mod 16 as its output, so the write-out is one TMA bulk store (plus at most
+    // two 8-byte words) that overlaps the next bin's count and scan (c5 local
+    // 7.52 -> 7.08 ms; with several bins per SM the thread stores are faster:
+    // c2 1.82 vs 1.86, kmc 12.9 vs 14.3 ms)
+    constexpr bool BULK = LB >= 512;
+    uint8_t* stg = BULK ? stage + ((uintptr_t)out & 15u) : stage;
     uint32_t d = sg.depth;
     const uint32_t W = local_width(n, wmax);
     const uint32_t nbk = 1u << W;
@@ -1208,7 +1241,9 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
       RS_PROF(0);
       if (!s_const) {
         local_scan<LB>(cnt, W, wsum);
-        __syncthreads();
+        if (pending && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        pending = false;
+        __syncthreads();  // starts in place; the stage is free
         RS_PROF(1);
         break;
       }
@@ -1265,7 +1300,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
         if (i * LB < lim) {
           const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
           const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-          st_rec<R>(stage + (size_t)(start_of(b) + rnk) * R, r[i]);
+          st_rec<R>(stg + (size_t)(start_of(b) + rnk) * R, r[i]);
           if (rnk == 1u) blist[slot++] = b;
         }
       }
@@ -1288,12 +1323,13 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
       RS_PROF(3);
       // the tail sorter's pivot path only in the small-bin configuration (duplicate-heavy
       // streams of small bins live there; the big-bin ones are short of registers)
-      tail = local_finish<R, K, LB, NW, LB == 64>(stage, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
-                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl
+      tail = local_finish<R, K, LB, NW, LB == 64>(stg, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
+                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl, BULK
 #ifdef RADSORT_PHASE_PROF
-                                       , false, pfl
+                                       , pfl
 #endif
       );
+      pending = BULK;
     }
     done += n;
     __syncthreads();
@@ -1304,6 +1340,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     bi = nb;
     sg = nsg;
   }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
 #ifdef RADSORT_PHASE_PROF
   if (tid == 0) {

@@ -20,7 +20,7 @@ struct Sorter {
     maxlen = std::min(maxlen, lmax);
     // smem: staged bin | 2^W u16 counters (aliased by the tail sorter's per-warp
     // scratch) | list of the buckets holding >= 2 records
-    const size_t stage_bytes = ((size_t)maxlen * R + 15) & ~(size_t)15;
+    const size_t stage_bytes = (((size_t)maxlen * R + 15) & ~(size_t)15) + 16;  // + the alignment shift
     const size_t tail_bytes = (LB / 32) * sizeof(TailScratch<K>);
     const uint32_t cap = maxlen / 2 + 1;  // buckets holding >= 2 records
     const size_t big_bytes = ((size_t)cap * 4 + 15) & ~(size_t)15;
