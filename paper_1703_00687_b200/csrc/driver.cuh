@@ -16,6 +16,7 @@
 #include "../../include/radsort.h"
 #include "passes.cuh"
 #include "local2.cuh"
+#include "local_pipe.cuh"
 
 namespace radsort {
 

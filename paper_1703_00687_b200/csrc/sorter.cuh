@@ -29,12 +29,27 @@ struct Sorter {
     while (wmax > LOCAL_WMIN && stage_bytes + cnt_of(wmax) + big_bytes > LOCAL_SMEM_MAX) --wmax;
     const size_t cnt_bytes = cnt_of(wmax);
     const size_t smem = stage_bytes + cnt_bytes + big_bytes;
+    if constexpr (LB == 512) {
+      if (pipe_on()) {  // one bin per SM: the bin-pipelined variant (k_local_pipe)
+        smem_attr(ctx, k_local_pipe<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
+        const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms);
+        k_local_pipe<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes,
+                                                         cap, next, nxt, ctl, recs, tmp, lmin, lmax);
+        return;
+      }
+    }
     smem_attr(ctx, k_local<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
     const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
     k_local<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt,
                                                ctl, recs, tmp, lmin, lmax);
+  }
+
+  // RADSORT_LOCAL_PIPE=0: the 512-thread local sort as k_local (round 1) instead of k_local_pipe
+  static bool pipe_on() {
+    const char* e = getenv("RADSORT_LOCAL_PIPE");
+    return !(e && e[0] == '0');
   }
 
   // ---- the largest local bins: k_local_big (1024 threads, one bin per SM) with
@@ -319,7 +334,9 @@ struct Sorter {
   static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v, bool lookback = false,
                                 uint32_t extra = 0) {
     const size_t capL = (size_t)n / C + 4 + extra;
-    const size_t capLoc = (size_t)n / (TINY_MAX + 1) + 4 + extra;
+    // Local bins: children of > TINY_MAX records, or mixed buckets of > ES_MAX records queued by
+    // the cluster / pipelined local sorts
+    const size_t capLoc = (size_t)n / (es_max<R>() + 1) + 4 + extra;
     const size_t tiles_max = (size_t)n / T + capL + 4;
     radsort_status rs;
     if ((rs = ensure(ctx->large[0], capL * sizeof(Seg)))) return rs;
