@@ -186,6 +186,23 @@ radsort_status radsort_sort_multi_loopback(void* group, int rank, void* dev_reco
 radsort_status radsort_plan_quotas(uint64_t N, int G, uint64_t* quotas);
 radsort_status radsort_plan_digit(const uint64_t* count_lt256, uint64_t q, uint32_t* digit);
 radsort_status radsort_plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, uint64_t* below);
+/* Fused-exchange plan (SURVEY.md §8(e) k_merge_scatter, §8(f) NEXT-3;
+ * PAPER.md:119-121 §3.1, the bins of the first digit processed independently):
+ *   all_tables   host, G*G*256*256 uint32: [sender][receiver][d0 bucket][digit
+ *                d0+1] = records of that sender's piece for that receiver with
+ *                those two digits (every rank's table, allgathered)
+ *   me           this rank; npieces, piece_dst[i] (receiver), piece_bucket[i]
+ *                (d0 bucket) describe this rank's pieces
+ *   piece_base   out, npieces*256 uint32: offset, in receiver piece_dst[i]'s
+ *                record buffer, of this rank's share of bin (piece_bucket[i], v);
+ *                receivers lay bins out in (d0, d0+1) order, senders in rank
+ *                order inside a bin
+ *   recv_off     out, 65537 uint64: offsets of rank me's 65536 bins; [65536] =
+ *                its record count
+ * INVALID_ARG on NULL / out-of-range arguments, CAPACITY when a receiver's
+ * count does not fit 32 bits.  Pure host function; the caller owns every buffer. */
+radsort_status radsort_plan_fused(const uint32_t* all_tables, int G, int me, uint32_t npieces, const uint32_t* piece_dst,
+                                  const uint32_t* piece_bucket, uint32_t* piece_base, uint64_t* recv_off);
 
 /* Splitter planning used by radsort_sort_multi (pure host function, exposed
  * for testing).  Given the GLOBAL (allreduced) 256-bin histogram `hist` of

@@ -61,6 +61,46 @@ static void plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, u
   }
 }
 
+// Fused exchange plan (step 6' below).  all[((src * G + r) * 256 + b) * 256 + v]
+// = records of sender src's piece for receiver r in d0 bucket b with digit
+// d0+1 = v (every rank's dense table, allgathered).  Receiver r lays its
+// (b, v) bins out in (b, v) order, senders in rank order inside a bin.
+// Outputs: base[i * 256 + v] = offset in receiver pdst[i]'s buffer of this
+// rank's share of bin (pbkt[i], v); recv_off[0..65536] = the bin offsets of
+// rank `me` (recv_off[65536] = its record count).  Returns false if a
+// receiver's total does not fit in 32 bits.
+static bool plan_fused(const uint32_t* all, int G, int me, uint32_t np, const uint32_t* pdst, const uint32_t* pbkt,
+                       uint32_t* base, uint64_t* recv_off, std::vector<uint64_t>* totals = nullptr) {
+  auto cnt = [&](int src, int r, size_t bv) { return all[((size_t)src * G + r) * 65536 + bv]; };
+  std::vector<char> need(G, 0);
+  for (uint32_t i = 0; i < np; ++i) need[pdst[i]] = 1;
+  need[me] = 1;
+  std::vector<std::vector<uint64_t>> roff(G);
+  for (int r = 0; r < G; ++r) {
+    if (!need[r]) continue;
+    roff[r].resize(65537);
+    uint64_t run = 0;
+    for (size_t bv = 0; bv < 65536; ++bv) {
+      roff[r][bv] = run;
+      for (int p = 0; p < G; ++p) run += cnt(p, r, bv);
+    }
+    roff[r][65536] = run;
+    if (run >> 32) return false;
+    if (totals) (*totals)[r] = run;
+  }
+  for (uint32_t i = 0; i < np; ++i) {
+    const int r = (int)pdst[i];
+    for (int v = 0; v < 256; ++v) {
+      const size_t bv = (size_t)pbkt[i] * 256 + v;
+      uint64_t o = roff[r][bv];
+      for (int p = 0; p < me; ++p) o += cnt(p, r, bv);
+      base[(size_t)i * 256 + v] = (uint32_t)o;
+    }
+  }
+  std::copy(roff[me].begin(), roff[me].end(), recv_off);
+  return true;
+}
+
 // -------------------------------------------------------------- transport
 enum class ROp { Sum, Min, Max };
 
@@ -418,40 +458,28 @@ static radsort_status fused_exchange(Transport& tr, Context* ctx, const LayoutOp
   if ((rs = tr.allgather(reinterpret_cast<const uint64_t*>(tab.data()), reinterpret_cast<uint64_t*>(all.data()),
                          E / 2, st)))
     return rs;
-  auto cnt = [&](int src, int r, size_t bv) { return all[(size_t)src * E + (size_t)r * 65536 + bv]; };
-  // offsets of the (b, v) bins in every receiver that one of my pieces goes to
-  std::vector<char> need(G, 0);
-  for (uint32_t i = 0; i < np; ++i) need[pdst[i]] = 1;
-  need[me] = 1;
-  std::vector<std::vector<uint64_t>> roff(G);
+  std::vector<uint32_t> hbase((size_t)np * 256);
+  std::vector<uint64_t> hdst(np), recv(65537), tot(G, 0);
+  if (!plan_fused(all.data(), G, me, np, pdst.data(), pbkt.data(), hbase.data(), recv.data(), &tot)) {
+    set_detail("fused exchange: a receiver's record count exceeds 2^32");
+    return RADSORT_ERR_CAPACITY;
+  }
   for (int r = 0; r < G; ++r) {
-    if (!need[r]) continue;
-    roff[r].resize(65537);
-    uint64_t run = 0;
-    for (size_t bv = 0; bv < 65536; ++bv) {
-      roff[r][bv] = run;
-      for (int p = 0; p < G; ++p) run += cnt(p, r, bv);
-    }
-    roff[r][65536] = run;
-    if (run != q[r]) {
-      set_detail("fused exchange: rank %d would receive %llu records, quota %llu", r, (unsigned long long)run,
+    if (tot[r] && tot[r] != q[r]) {
+      set_detail("fused exchange: rank %d would receive %llu records, quota %llu", r, (unsigned long long)tot[r],
                  (unsigned long long)q[r]);
       return RADSORT_ERR_CUDA;
     }
   }
-  std::vector<uint32_t> hbase((size_t)np * 256);
-  std::vector<uint64_t> hdst(np);
+  if (recv[65536] != q[me]) {
+    set_detail("fused exchange: %llu records received, quota %llu", (unsigned long long)recv[65536],
+               (unsigned long long)q[me]);
+    return RADSORT_ERR_CUDA;
+  }
   uint64_t sent = 0;
   for (uint32_t i = 0; i < np; ++i) {
-    const int r = (int)pdst[i];
-    for (int v = 0; v < 256; ++v) {
-      const size_t bv = (size_t)pbkt[i] * 256 + v;
-      uint64_t o = roff[r][bv];
-      for (int p = 0; p < me; ++p) o += cnt(p, r, bv);
-      hbase[(size_t)i * 256 + v] = (uint32_t)o;
-    }
-    hdst[i] = (uint64_t)(uintptr_t)peer[r];
-    if (r != me) sent += plen[i];
+    hdst[i] = (uint64_t)(uintptr_t)peer[pdst[i]];
+    if ((int)pdst[i] != me) sent += plen[i];
   }
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -462,14 +490,14 @@ static radsort_status fused_exchange(Transport& tr, Context* ctx, const LayoutOp
   std::vector<uint32_t> seg_off, seg_len;
   uint64_t recv_other = 0;
   for (size_t bv = 0; bv < 65536; ++bv) {
-    const uint64_t len = roff[me][bv + 1] - roff[me][bv];
+    const uint64_t len = recv[bv + 1] - recv[bv];
     if (len) {
-      seg_off.push_back((uint32_t)roff[me][bv]);
+      seg_off.push_back((uint32_t)recv[bv]);
       seg_len.push_back((uint32_t)len);
     }
-    recv_other += len - cnt(me, me, bv);
+    recv_other += len - all[((size_t)me * G + me) * 65536 + bv];
   }
-  const uint64_t got = roff[me][65536];
+  const uint64_t got = recv[65536];
   stats.nvlink_bytes_sent = sent * R;
   stats.nvlink_bytes_recv = recv_other * R;
   radsort_stats sub = {};
@@ -859,6 +887,17 @@ radsort_status radsort_plan_digit(const uint64_t* count_lt256, uint64_t q, uint3
   if (!count_lt256 || !digit || count_lt256[0] > q) return RADSORT_ERR_INVALID_ARG;
   *digit = plan_digit(count_lt256, q);
   return RADSORT_OK;
+}
+
+radsort_status radsort_plan_fused(const uint32_t* all_tables, int G, int me, uint32_t npieces, const uint32_t* piece_dst,
+                                  const uint32_t* piece_bucket, uint32_t* piece_base, uint64_t* recv_off) {
+  if (!all_tables || G < 1 || me < 0 || me >= G || (npieces && (!piece_dst || !piece_bucket || !piece_base)) ||
+      !recv_off)
+    return RADSORT_ERR_INVALID_ARG;
+  for (uint32_t i = 0; i < npieces; ++i)
+    if ((int)piece_dst[i] >= G || piece_bucket[i] > 255) return RADSORT_ERR_INVALID_ARG;
+  return plan_fused(all_tables, G, me, npieces, piece_dst, piece_bucket, piece_base, recv_off) ? RADSORT_OK
+                                                                                                 : RADSORT_ERR_CAPACITY;
 }
 
 radsort_status radsort_plan_equal_split(const uint64_t* e, int G, uint64_t L, uint64_t Q, uint64_t* below) {

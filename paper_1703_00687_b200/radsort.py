@@ -22,7 +22,7 @@ EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_mu
            "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
            "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench",
            "radsort_unique_count", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy",
-           "radsort_tinysort"]
+           "radsort_tinysort", "radsort_plan_fused"]
 
 
 class Stats(ctypes.Structure):
@@ -73,13 +73,14 @@ def _load():
     L.radsort_plan_quotas.argtypes = [u64, i32, vp]
     L.radsort_plan_digit.argtypes = [vp, u64, ctypes.POINTER(u32)]
     L.radsort_plan_equal_split.argtypes = [vp, i32, u64, u64, vp]
+    L.radsort_plan_fused.argtypes = [vp, i32, i32, u32, vp, vp, vp, vp]
     L.radsort_tinybench.argtypes = [u32, u32, u32, u32, u64, ctypes.POINTER(ctypes.c_double)]
     L.radsort_unique_count.argtypes = [vp, u64, u32, u32, vp, vp, ctypes.POINTER(u64), vp]
     L.radsort_tinysort.argtypes = [u32, u32, u32, u32, vp, vp, u64, vp]
     L.radsort_comm_get_unique_id.argtypes = [vp]
     L.radsort_comm_init.argtypes = [vp, i32, i32, i32, ctypes.POINTER(vp)]
     L.radsort_comm_destroy.argtypes = [vp]
-    for f in ("radsort_tinysort", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
+    for f in ("radsort_plan_fused", "radsort_tinysort", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
               "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
               "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split",
               "radsort_tinybench", "radsort_unique_count"):
@@ -239,6 +240,24 @@ def plan_equal_split(e, L: int, Q: int):
     _check(lib.radsort_plan_equal_split(ctypes.c_void_p(e.ctypes.data), len(e), L, Q,
                                         ctypes.c_void_p(below.ctypes.data)))
     return below
+
+
+def plan_fused(all_tables, me: int, piece_dst, piece_bucket):
+    """Fused-exchange plan (radsort_plan_fused): all_tables = every rank's dense
+    piece histogram table, uint32 [G, G, 256, 256] (sender, receiver, d0 bucket,
+    digit d0+1).  Returns (piece_base [npieces, 256], recv_off [65537])."""
+    import numpy as np
+
+    t = np.ascontiguousarray(all_tables, dtype=np.uint32)
+    G = t.shape[0]
+    pd = np.ascontiguousarray(piece_dst, dtype=np.uint32)
+    pb = np.ascontiguousarray(piece_bucket, dtype=np.uint32)
+    base = np.zeros((len(pd), 256), dtype=np.uint32)
+    recv = np.zeros(65537, dtype=np.uint64)
+    _check(lib.radsort_plan_fused(ctypes.c_void_p(t.ctypes.data), G, me, len(pd), ctypes.c_void_p(pd.ctypes.data),
+                                  ctypes.c_void_p(pb.ctypes.data), ctypes.c_void_p(base.ctypes.data),
+                                  ctypes.c_void_p(recv.ctypes.data)))
+    return base, recv
 
 
 def locate_bucket(hist256, q: int):

@@ -7,7 +7,10 @@ radsort_plan_digit / radsort_plan_equal_split.  Here two gloo ranks drive
 exactly those functions over real collectives (numpy stands in for the device
 histogram / binary-search kernels, which tests/test_gpu_multi.py covers on the
 GPU), exchange their slices, and the rank-order concatenation is checked
-against the oracle and the exact quotas."""
+against the oracle and the exact quotas.  With fused=True the exchange is the
+fused one: radsort_plan_fused places every record of every piece in its
+receiver's (d0, d0+1) bin, and the receivers' buffers must come out exactly
+covered."""
 import os
 import socket
 
@@ -49,7 +52,7 @@ def _allgather(x):
     return np.stack([o.numpy() for o in out]).view(np.uint64)
 
 
-def _worker(rank, world, port, dist_name, result_q):
+def _worker(rank, world, port, dist_name, result_q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -108,10 +111,52 @@ def _worker(rank, world, port, dist_name, result_q):
         below = rs.plan_equal_split(allv[:, 1], L, Qg)
         cuts.append(lo + lt + int(below[rank]))
     cuts.append(len(keys))
-    # exchange (every rank's slice for every destination), then sort the received key range
-    allp = [None] * G
-    dist.all_gather_object(allp, [part[cuts[g]:cuts[g + 1]] for g in range(G)])
-    mine = np.concatenate([allp[src][rank] for src in range(G)])
+    if not fused:
+        # exchange (every rank's slice for every destination), then sort the received key range
+        allp = [None] * G
+        dist.all_gather_object(allp, [part[cuts[g]:cuts[g + 1]] for g in range(G)])
+        mine = np.concatenate([allp[src][rank] for src in range(G)])
+    else:
+        # fused exchange (radsort_plan_fused): pieces = (receiver, d0 bucket) ranges of the
+        # partitioned array, histogrammed by digit d0+1; every record is "stored" at
+        # base[piece][v] + its rank among the piece's records with digit v (the k_scatter<PEER>
+        # pass); the receiver's buffer must come out exactly covered, bin (b, v) by bin
+        d1 = d0 + 1
+        pdst, pbkt, prng = [], [], []
+        for g in range(G):
+            for b in range(256):
+                lo, hi = max(cuts[g], int(lbase[b])), min(cuts[g + 1], int(lbase[b + 1]))
+                if hi > lo:
+                    pdst.append(g)
+                    pbkt.append(b)
+                    prng.append((lo, hi))
+        tab = np.zeros((G, 256, 256), dtype=np.uint32)
+        for g, b, (lo, hi) in zip(pdst, pbkt, prng):
+            tab[g, b] = np.bincount(_digit(pkeys[lo:hi], d1), minlength=256)
+        tabs = [None] * G
+        dist.all_gather_object(tabs, tab)
+        base, recv = rs.plan_fused(np.stack(tabs), rank, pdst, pbkt)
+        sends = [[] for _ in range(G)]
+        for i, (g, (lo, hi)) in enumerate(zip(pdst, prng)):
+            dv = _digit(pkeys[lo:hi], d1)
+            o = np.argsort(dv, kind="stable")
+            rank_in = np.empty(hi - lo, dtype=np.int64)
+            rank_in[o] = np.arange(hi - lo) - np.searchsorted(dv[o], dv[o], "left")
+            sends[g].append((base[i][dv].astype(np.int64) + rank_in, part[lo:hi]))
+        allsends = [None] * G
+        dist.all_gather_object(allsends, sends)
+        n_recv = int(recv[65536])
+        mine = np.zeros((n_recv, a.shape[1]), dtype=a.dtype)
+        hits = np.zeros(n_recv, dtype=np.int64)
+        for src in range(G):
+            for off, recs in allsends[src][rank]:
+                mine[off] = recs
+                np.add.at(hits, off, 1)
+        assert (hits == 1).all(), "fused exchange plan left gaps or overlaps"
+        mk0 = mine.view(np.uint64).reshape(-1, 2)[:, 0]
+        bv = _digit(mk0, d0) * 256 + _digit(mk0, d1)
+        assert (np.diff(bv) >= 0).all(), "records outside their (d0, d0+1) bin"
+        assert (np.searchsorted(bv, np.arange(65536), "left") == recv[:65536].astype(np.int64)).all()
     assert mine.shape[0] == int(q[rank]), (mine.shape, q)
     mk = mine.view(np.uint64).reshape(-1, 2)[:, 0]
     mine = mine[np.argsort(mk, kind="stable")]
@@ -129,11 +174,12 @@ def _worker(rank, world, port, dist_name, result_q):
 
 
 @pytest.mark.parametrize("dist_name", ["uniform40", "few", "equal", "bytes"])
-def test_two_rank_plan_matches_oracle(dist_name):
+@pytest.mark.parametrize("fused", [False, True])
+def test_two_rank_plan_matches_oracle(dist_name, fused):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, dist_name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, dist_name, q, fused)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
