@@ -329,7 +329,7 @@ def run_radsort(args):
         with open(tp) as f:
             traffic_map = json.load(f)
     names = {"scatter": "k_scatter (radix pass: rank, smem staging, coalesced scatter)",
-             "local": "k_local + k_local_cluster (on-chip sort of bins <= C records / of C < n <= ~4C records "
+             "local": "k_local / k_local_pipe + k_local_cluster (on-chip sort of bins <= C records / of C < n <= ~4C records "
                       "in a 4-CTA cluster)",
              "hist": "k_hist_pre (digit histogram + per-tile prefix, read only)"}
     launches_per_step = {k: v for k, v in rs.last_stats()["kernel_launches"].items()}

@@ -23,7 +23,7 @@ template <int R, int K, int IL, int LB>
 __global__ void __launch_bounds__(LB, 1)
     k_local_pipe(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes,
                  uint32_t cnt_bytes, uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
-                 uint32_t lmin, uint32_t lmax) {
+                 uint32_t lmin, uint32_t lmax, int wdelta) {
   extern __shared__ uint4 smem_raw[];
   constexpr int KW = K / 8;
   constexpr int NW = LB / 32;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(LB, 1)
     uint8_t* out = recs + (size_t)sg.off * R;
     uint8_t* stg = stage + ((uintptr_t)out & 15u);
     uint32_t d = sg.depth;
-    const uint32_t W = local_width(n, wmax);
+    const uint32_t W = (uint32_t)max((int)LOCAL_WMIN, min((int)wmax, (int)local_width(n, wmax) + wdelta));
     const uint32_t nbk = 1u << W;
     uint32_t rk[IP];
     uint32_t ones = 0;

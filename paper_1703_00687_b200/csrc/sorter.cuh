@@ -34,7 +34,7 @@ struct Sorter {
         smem_attr(ctx, k_local_pipe<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
         const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms);
         k_local_pipe<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes,
-                                                         cap, next, nxt, ctl, recs, tmp, lmin, lmax);
+                                                         cap, next, nxt, ctl, recs, tmp, lmin, lmax, wdelta());
         return;
       }
     }
@@ -47,6 +47,11 @@ struct Sorter {
   }
 
   // RADSORT_LOCAL_PIPE=0: the 512-thread local sort as k_local (round 1) instead of k_local_pipe
+  // RADSORT_LOCAL_WDELTA: composite digit width of k_local_pipe relative to ceil(log2 n) + 1 (experiments)
+  static int wdelta() {
+    const char* e = getenv("RADSORT_LOCAL_WDELTA");
+    return e ? atoi(e) : 0;
+  }
   static bool pipe_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE");
     return !(e && e[0] == '0');
