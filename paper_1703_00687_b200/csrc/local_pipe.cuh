@@ -234,9 +234,8 @@ __global__ void __launch_bounds__(LB, 1)
         if (i * LB < lim) {
           const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
           const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-          const uint32_t s0 = start16[b];
-          st_rec<R>(stg + (size_t)(s0 + rnk) * R, r[i]);
-          if (rnk == 1u && fix) blist[slot++] = s0 | (((b + 1 < nbk ? (uint32_t)start16[b + 1] : n) - s0) << 16);
+          st_rec<R>(stg + (size_t)(start16[b] + rnk) * R, r[i]);
+          if (rnk == 1u && fix) blist[slot++] = b;  // the bucket; turned into start | count below
         }
       }
     }
@@ -250,7 +249,7 @@ __global__ void __launch_bounds__(LB, 1)
     }
     prefetch_l2(nb + gridDim.x);
     done += n;
-    __syncthreads();  // staged; counters (starts) consumed
+    __syncthreads();  // staged
     if (!all_equal) {
       p_live = true;
       p_stg = stg;
@@ -259,6 +258,12 @@ __global__ void __launch_bounds__(LB, 1)
       p_ncol = s_ncol[q];
       p_off = sg.off;
       p_nd = d + (W >= 16 ? 2u : 1u);
+      // collision list: bucket -> start | count << 16 (the counters are reused by the next bin)
+      for (uint32_t e = tid; e < p_ncol; e += LB) {
+        const uint32_t b = blist[e], s0 = start16[b];
+        blist[e] = s0 | (((b + 1 < nbk ? (uint32_t)start16[b + 1] : n) - s0) << 16);
+      }
+      __syncthreads();  // starts consumed
     }
     par = q;
     zero_cnt(2u << W);
