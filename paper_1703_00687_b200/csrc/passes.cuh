@@ -605,11 +605,24 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     sh_s = t < total ? (tile_seg ? __ldg(tile_seg + t) : seg_of_tile(tile_start, nseg, t)) : 0u;
   };
   Rec<R> r[I];
+  // reduce-then-scan offsets of the loaded tile (PRE), loaded with its records
+  // and summed only when the tile is processed, so no warp waits on them
+  uint32_t q_tp = 0, q_sb = 0, q_cf = 0, q_ci = 0;
+  const uint32_t per = PRE ? (total + hist_grid - 1) / hist_grid : 1u;
   // issue this tile's loads into r[] (software pipelining: the loads of tile
   // k+1 are in flight while tile k is looked back and written out)
   auto load = [&](uint32_t t, uint32_t s) {
     const Seg sg = segs[s];
     if (sg.mode != MODE_SCATTER && sg.mode != MODE_SPLIT) return;  // split tiles: a cache-warming prefetch
+    if constexpr (PRE && R >= 16) {  // (R = 8 measured 0.5 % slower: registers)
+      if (sg.mode == MODE_SCATTER && tid < RADIX) {
+        const uint32_t ch = t / per;
+        q_tp = __ldg(tile_pre + (size_t)t * RADIX + tid);
+        q_sb = __ldg(segbase + (size_t)s * RADIX + tid);
+        q_cf = __ldg(ch_first + ch);
+        q_ci = __ldg(carry_in + (size_t)ch * RADIX + tid);
+      }
+    }
     const uint32_t lt = t - tile_start[s];
     const uint32_t m = min(T, sg.len - lt * T);
     const uint8_t* src = buf_of(sg.src, recs, tmp) + (size_t)(sg.off + lt * T) * R;
@@ -640,20 +653,13 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     if (sg.mode == MODE_SCATTER) {
       const uint32_t d = sg.depth;
       uint32_t pre_excl = 0;
-      if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry) + bin base, loaded early
-        if (tid < RADIX) {
-          const uint32_t per = (total + hist_grid - 1) / hist_grid;
+      if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry) + bin base, loaded with the tile
+        if constexpr (R >= 16) {
+          if (tid < RADIX) pre_excl = q_tp + q_sb + (s == q_cf ? q_ci : 0u);
+        } else if (tid < RADIX) {
           const uint32_t ch = t / per;
-          if constexpr (R >= 24) {
-            // four independent loads (the carry is selected after they land, not loaded behind
-            // ch_first): c4 scatter 25.4 -> 24.0 ms; R <= 16 measured 1 % slower this way
-            const uint32_t cf = __ldg(ch_first + ch), ci = __ldg(carry_in + (size_t)ch * RADIX + tid);
-            pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
-                       (s == cf ? ci : 0u);
-          } else {
-            pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
-                       (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
-          }
+          pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
+                     (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
         }
       }
       uint32_t rk[(I + 1) / 2];  // ranks < T <= 2^16: two per register (fewer live registers under the cap)
