@@ -23,7 +23,8 @@ __device__ __forceinline__ uint64_t uw(uint64_t seed, uint64_t i, int w, int W) 
   return mix64(seed + ((uint64_t)W * i + (uint64_t)(w + 1)) * GOLDEN);
 }
 
-// Zipf rejection-inversion (Hoermann & Derflinger), same constants as host.py
+// Zipf rejection-inversion (Hoermann & Derflinger, ACM TOMACS 1996; helper1/2 in
+// the form Apache Commons Math publishes), same constants as host.py
 __device__ __forceinline__ double helper1(double x) {
   return fabs(x) > 1e-8 ? log1p(x) / x : 1.0 - x * (0.5 - x * (1.0 / 3.0 - 0.25 * x));
 }

@@ -84,6 +84,10 @@ def u(seed: int, idx, w: int, W: int = W_DEFAULT):
 
 
 # ---- Zipf (Hoermann & Derflinger rejection-inversion), double precision ----
+# Source: W. Hoermann, G. Derflinger, "Rejection-inversion to generate variates
+# from monotone discrete distributions", ACM TOMACS 6(3), 1996; the helper1 /
+# helper2 Taylor fallbacks follow the form Apache Commons Math publishes
+# (RejectionInversionZipfSampler).  Test/bench input generator only.
 def _helper1(x):
     x = np.asarray(x, dtype=np.float64)
     small = np.abs(x) <= 1e-8
