@@ -131,6 +131,12 @@ __global__ void __launch_bounds__(LB, 1)
   if (tid == 0) s_const = 0;
   unsigned long long done = 0;
   constexpr int IP = (IL + 1) / 2;
+#ifdef RADSORT_PHASE_PROF
+  unsigned long long pf[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tA = clock64(), tB = 0;
+#define RS_PROF(i) do { if (tid == 0) { tB = clock64(); pf[i] += tB - tA; tA = tB; } } while (0)
+#else
+#define RS_PROF(i) do { } while (0)
+#endif
   for (;;) {
     const uint32_t n = sg.len;
     const int lim = (int)n - tid;
@@ -169,16 +175,21 @@ __global__ void __launch_bounds__(LB, 1)
       if (first && p_live) fixup();  // the previous bin, behind the atomics
       if (cst) s_const = 1u;
       __syncthreads();
+      RS_PROF(0);
       if (first && p_live) {
         finish();  // big buckets, bulk store (contains a barrier when it stores)
         p_live = false;
       }
       first = false;
+      RS_PROF(1);
       if (!s_const) {
         local_scan<LB>(cnt, W, wsum);
+        RS_PROF(2);
         if (pending && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         pending = false;
+        RS_PROF(3);
         __syncthreads();  // starts in place; the stage is free
+        RS_PROF(4);
         break;
       }
       // every record in one bucket: skip the constant digits
@@ -249,7 +260,9 @@ __global__ void __launch_bounds__(LB, 1)
     }
     prefetch_l2(nb + gridDim.x);
     done += n;
+    RS_PROF(5);
     __syncthreads();  // staged
+    RS_PROF(6);
     if (!all_equal) {
       p_live = true;
       p_stg = stg;
@@ -267,6 +280,7 @@ __global__ void __launch_bounds__(LB, 1)
     }
     par = q;
     zero_cnt(2u << W);
+    RS_PROF(7);
     if (nb >= nlist) break;
     bi = nb;
     sg = nsg;
@@ -279,6 +293,11 @@ __global__ void __launch_bounds__(LB, 1)
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (tid == 0) atomicAdd(&ctl->rec_local, done);
+#ifdef RADSORT_PHASE_PROF
+  if (tid == 0)
+    for (int q = 0; q < 8; ++q) atomicAdd(&ctl->prof[8 + q], pf[q]);
+#endif
+#undef RS_PROF
 }
 
 }  // namespace radsort

@@ -30,7 +30,9 @@ struct Sorter {
     const size_t cnt_bytes = cnt_of(wmax);
     const size_t smem = stage_bytes + cnt_bytes + big_bytes;
     if constexpr (LB == 512) {
-      if (pipe_on()) {  // one bin per SM: the bin-pipelined variant (k_local_pipe)
+      // one bin per SM: the bin-pipelined variant (k_local_pipe).  Measured and dropped: the
+      // same at 1024 threads (c5 local 6.74 -> 6.52 ms but c3 5.06 -> 5.23 ms, 18 B of spills)
+      if (pipe_on()) {
         smem_attr(ctx, k_local_pipe<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
         const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms);
         k_local_pipe<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes,
@@ -38,6 +40,14 @@ struct Sorter {
         return;
       }
     }
+    if constexpr (LB <= 512) launch_local_k<IL, LB>(ctx, nloc, list, next, nxt, ctl, recs, tmp, lmin, lmax, wmax,
+                                                   stage_bytes, cnt_bytes, cap, smem, st);
+  }
+  template <int IL, int LB>
+  static void launch_local_k(Context* ctx, uint32_t nloc, const Seg* list, Seg* next, int nxt, Ctl* ctl, uint8_t* recs,
+                             uint8_t* tmp, uint32_t lmin, uint32_t lmax, uint32_t wmax, size_t stage_bytes,
+                             size_t cnt_bytes, uint32_t cap, size_t smem, cudaStream_t st) {
+    const int sms = ctx->sms;
     smem_attr(ctx, k_local<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local<R, K, IL, LB>, LB, smem);
@@ -56,6 +66,7 @@ struct Sorter {
     const char* e = getenv("RADSORT_LOCAL_PIPE");
     return !(e && e[0] == '0');
   }
+
 
   // ---- the largest local bins: k_local_big (1024 threads, one bin per SM) with
   // RADSORT_LOCAL_BIG=1; k_local at 512 threads otherwise
