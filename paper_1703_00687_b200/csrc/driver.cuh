@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (ranges show in nsys / ncu when a tool is attached)
+
 #include "../../include/radsort.h"
 #include "passes.cuh"
 #include "local2.cuh"
@@ -82,7 +84,21 @@ inline void smem_attr(Context* ctx, F* f, int bytes) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-// per-kernel-class CUDA-event timing on the sort's stream (radsort_set_timing)
+// NVTX range for the host-side phases (the MSD level, the multi-GPU steps)
+struct NvtxRange {
+  explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+inline const char* kernel_class_name(int k) {
+  static const char* names[RADSORT_K_COUNT] = {"radsort sample", "radsort hist",  "radsort plan",   "radsort scatter",
+                                               "radsort children", "radsort local", "radsort multi", "radsort gather"};
+  return (k >= 0 && k < RADSORT_K_COUNT) ? names[k] : "radsort";
+}
+
+// per-kernel-class CUDA-event timing on the sort's stream (radsort_set_timing),
+// and an NVTX range per kernel class
 struct Timer {
   Context* ctx;
   cudaStream_t st;
@@ -91,11 +107,13 @@ struct Timer {
   bool on;
   Timer(Context* c, cudaStream_t s) : ctx(c), st(s), on(g_timing) {}
   void begin(int k) {
+    nvtxRangePushA(kernel_class_name(k));
     if (!on || n >= 64) return;
     cls[n] = k;
     cudaEventRecord(ctx->ev[2 * n], st);
   }
   void end() {
+    nvtxRangePop();
     if (!on || n >= 64) return;
     cudaEventRecord(ctx->ev[2 * n + 1], st);
     ++n;

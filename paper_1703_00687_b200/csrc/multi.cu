@@ -443,6 +443,7 @@ static radsort_status fused_exchange(Transport& tr, Context* ctx, const LayoutOp
       }
     }
   const uint32_t np = (uint32_t)poff.size();
+  NvtxRange nvtx_fx("radsort multi: fused exchange");
   PieceWs w;
   std::vector<uint32_t> ph((size_t)np * 256);
   {
@@ -571,6 +572,7 @@ static radsort_status sort_multi_impl(Transport& tr, uint8_t* recs, uint8_t* tmp
   const uint32_t n = (uint32_t)n_local;
 
   // 2. global first non-constant digit and its histogram
+  NvtxRange nvtx_plan("radsort multi: histogram + splitters");
   uint64_t h[256], ao[4];
   auto hist_op = [&](uint32_t digit) {
     std::lock_guard<std::mutex> lk(ctx->mu);

@@ -501,7 +501,11 @@ struct Sorter {
     }
     int cur = 0;
     const int max_levels = 2 * K + 4;
+    static const char* level_names[] = {"radsort level 0", "radsort level 1", "radsort level 2", "radsort level 3",
+                                        "radsort level 4", "radsort level 5", "radsort level 6", "radsort level 7",
+                                        "radsort level 8+"};
     for (int level = 0;; ++level) {
+      NvtxRange nvtx_level(level_names[level < 8 ? level : 8]);
       if (level > max_levels) {
         set_detail("MSD level loop did not terminate (%d levels)", level);
         return RADSORT_ERR_CUDA;
