@@ -82,6 +82,8 @@ typedef struct {
   uint32_t exchange;          /* multi-GPU: 1 = send/recv exchange, 2 = fused exchange
                                  (next-digit scatter straight into the peers' buffers) */
   uint32_t key_index;         /* 1: sorted as (key, index) records + one payload gather */
+  uint32_t wide_levels;       /* levels that scattered by a 10-bit digit (digit d plus the
+                                 two leading bits of digit d+1; DESIGN.md §3 "wide level") */
 } radsort_stats;
 
 /* Create the per-(process, device) context for `device` (cudaSetDevice is the

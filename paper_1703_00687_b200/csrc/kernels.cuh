@@ -29,6 +29,13 @@ template <int R, int TB, int SB> __host__ __device__ constexpr uint32_t tile_rec
 enum : uint8_t { SRC_REC = 0, SRC_TMP = 1 };
 enum : uint8_t { MODE_NONE = 0, MODE_SCATTER = 1, MODE_COPY = 2, MODE_SPLIT = 3, MODE_FILL = 4 };
 enum : uint8_t { FLAG_EQUAL = 1, FLAG_FILL = 2, FLAG_CAND = 4 };  // CAND: sampled as possibly key-dominated
+// Bits [4, 7) of Seg::flags: how many leading bits of digit `depth` the bin's
+// keys already share (2 for the children of a 10-bit pass, DESIGN.md §3 "wide
+// level"; 0 otherwise).  Only the CTA-local sorters read it (their composite
+// digit starts below the shared bits); every other step is correct without it.
+constexpr int FLAG_SKIP_SHIFT = 4;
+constexpr uint8_t FLAG_SKIP_MASK = 7u << FLAG_SKIP_SHIFT;
+__host__ __device__ __forceinline__ uint32_t seg_skip(uint8_t flags) { return (flags >> FLAG_SKIP_SHIFT) & 7u; }
 
 // A bin ("bins that may be further processed independently"):
 // record range [off, off+len) of buffer `src`, to be partitioned by digit `depth`.
@@ -58,6 +65,7 @@ struct Ctl {
   uint32_t n_probe;                          // probe-key table entries used this sort
   uint32_t n_local_small[2];                 // Local list entries of <= small_cap<R>() records (by parity)
   uint32_t n_local_med[2];                   // ... of small_cap < len <= med_cap<R>() records
+  unsigned long long rec_large_next;          // records of the entries appended to Large[nxt] this level
   unsigned long long prof[16];  // phase cycle counters (RADSORT_PHASE_PROF builds only)
 };
 
@@ -171,6 +179,27 @@ __device__ __forceinline__ uint32_t digit_of(const Key<16>& k, uint32_t d) {
   return d < 8 ? (uint32_t)(k.w1 >> (8u * (7u - d))) & 255u : (uint32_t)(k.w0 >> (8u * (15u - d))) & 255u;
 }
 
+// 1 <= W <= 32 key bits starting sb < 8K bits below the most significant one
+// (zero bits past the end of the key).
+__device__ __forceinline__ uint32_t key_bits(const Key<8>& k, uint32_t sb, uint32_t W) {
+  return (uint32_t)((k.w0 << sb) >> (64u - W));
+}
+__device__ __forceinline__ uint32_t key_bits(const Key<16>& k, uint32_t sb, uint32_t W) {
+  uint64_t x;
+  if (sb == 0) x = k.w1;
+  else if (sb < 64) x = (k.w1 << sb) | (k.w0 >> (64u - sb));
+  else x = k.w0 << (sb - 64u);
+  return (uint32_t)(x >> (64u - W));
+}
+// The radix digit of a pass of DB bits at depth d: DB = 8 is digit d (one key
+// byte); DB = 10 is digit d followed by the two leading bits of
+// digit d+1 (a "wide" level).
+template <int DB, int K>
+__device__ __forceinline__ uint32_t digit_w(const Key<K>& k, uint32_t d) {
+  if constexpr (DB == 8) return digit_of(k, d);
+  else return key_bits(k, 8u * d, (uint32_t)DB);
+}
+
 // First digit >= d whose byte differs between the AND and the OR of all keys
 // of a bin (i.e. the first non-constant digit, "bins ... tend to
 // shrink (except bins with all keys equal)"); returns K if none.
@@ -251,6 +280,39 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* ws)
   }
   __syncthreads();
   return x - v + add;
+}
+
+// Exclusive scan of one value per thread over a block of NT threads (every
+// thread calls it; it contains barriers).  `ws` = NT/32 words of smem.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* ws) {
+  if constexpr (NT == 256) {
+    return block_excl_scan256(v, ws);
+  } else {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t t = lane < NW ? ws[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      if (lane < NW) ws[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t add = w > 0 ? ws[w - 1] : 0u;
+    __syncthreads();
+    return x - v + add;
+  }
 }
 
 // ------------------------------------------------------- warp tiny sorter

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(LB, 1)
     uint8_t* out = recs + (size_t)sg.off * R;
     uint8_t* stg = stage + ((uintptr_t)out & 15u);
     uint32_t d = sg.depth;
+    uint32_t sk = seg_skip(sg.flags);  // leading bits of digit d the bin already shares
     const uint32_t W = (uint32_t)max((int)LOCAL_WMIN, min((int)wmax, (int)local_width(n, wmax) + wdelta));
     const uint32_t nbk = 1u << W;
     uint32_t rk[IP];
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(LB, 1)
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
           const uint32_t sh = 16u * (b & 1u);
           const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
           rk[i >> 1] |= old << (16 * (i & 1));
@@ -220,10 +221,11 @@ __global__ void __launch_bounds__(LB, 1)
       __syncthreads();
       if (d2 >= (uint32_t)K) { all_equal = true; break; }
       d = d2;
+      sk = 0;
     }
     const uint32_t q = par ^ 1u;  // this bin's list parity
     const uint16_t* start16 = reinterpret_cast<const uint16_t*>(cnt);
-    const bool fix = 8 * ((int)K - (int)d) > (int)W;  // key bits left below the composite digit
+    const bool fix = 8 * ((int)K - (int)d) - (int)sk > (int)W;  // key bits left below the composite digit
     if (all_equal) {  // final where it is (copied out of tmp)
       if (sg.src == SRC_TMP) {
 #pragma unroll
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(LB, 1)
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
           const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
           st_rec<R>(stg + (size_t)(start16[b] + rnk) * R, r[i]);
           if (rnk == 1u && fix) blist[slot++] = b;  // the bucket; turned into start | count below
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(LB, 1)
       p_n = n;
       p_ncol = s_ncol[q];
       p_off = sg.off;
-      p_nd = d + (W >= 16 ? 2u : 1u);
+      p_nd = d + (sk + W) / 8u;  // digits shared by a bucket's keys
       // collision list: bucket -> start | count << 16 (the counters are reused by the next bin)
       for (uint32_t e = tid; e < p_ncol; e += LB) {
         const uint32_t b = blist[e], s0 = start16[b];

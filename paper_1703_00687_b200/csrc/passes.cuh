@@ -129,6 +129,7 @@ static __global__ void k_prep(const Seg* __restrict__ segs, uint32_t nseg, uint3
     ctl->tiles_total = run;
     ctl->scatter_ticket = 0;
     ctl->n_large_next = 0;
+    ctl->rec_large_next = 0;
     ctl->n_local[nxt] = 0;
     ctl->n_local_small[nxt] = 0;
     ctl->n_local_med[nxt] = 0;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(HIST_B) k_hist(const Seg* __restrict__ segs, c
 // and ch_tot[c][v] = count of digit v of the chunk's last segment in the chunk
 // (k_carry turns these into each chunk's carry-in).
 constexpr uint32_t NO_SEG = 0xffffffffu;
-template <int R, int K, uint32_t T>
+template <int R, int K, uint32_t T, int DB = 8>
 __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                      uint32_t nseg, const Ctl* __restrict__ ctl,
                                                      uint32_t* __restrict__ hist, unsigned long long* __restrict__ andor,
@@ -259,8 +260,9 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
                                                      uint32_t* __restrict__ ch_first, uint32_t* __restrict__ ch_last,
                                                      uint32_t* __restrict__ ch_tot, const uint32_t* __restrict__ tile_seg) {
   constexpr int KW = K / 8;
+  constexpr int DG = 1 << DB;  // digits of the pass (256, or 1024 on a wide level)
   constexpr int U = R <= 8 ? 16 : 8;  // keys in flight per thread
-  __shared__ uint32_t h[RADIX], run[RADIX];
+  __shared__ uint32_t h[DG], run[DG];
   __shared__ unsigned long long sna[2], so[2];
   const uint32_t total = ctl->tiles_total;
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
     if (tid == 0) ch_first[c] = ch_last[c] = NO_SEG;
     return;
   }
-  for (int i = tid; i < RADIX; i += HIST_B) h[i] = run[i] = 0;
+  for (int i = tid; i < DG; i += HIST_B) h[i] = run[i] = 0;
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
   __syncthreads();
   uint64_t na[2] = {0, 0}, o[2] = {0, 0};
@@ -301,8 +303,8 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
       o[w] = 0;
     }
     __syncthreads();
-    for (int i = tid; i < RADIX; i += HIST_B) {
-      if (run[i]) atomicAdd(&hist[(size_t)s * RADIX + i], run[i]);
+    for (int i = tid; i < DG; i += HIST_B) {
+      if (run[i]) atomicAdd(&hist[(size_t)s * DG + i], run[i]);
       run[i] = 0;
     }
     if (tid < KW) {
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
         for (int u = 0; u < U; ++u) {
           const uint32_t i = i0 + u * HIST_B;
           if (i < m) {
-            atomicAdd(&h[digit_of(k[u], d)], 1u);
+            atomicAdd(&h[digit_w<DB>(k[u], d)], 1u);
             na[0] |= ~k[u].w0; o[0] |= k[u].w0;
             if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
           }
@@ -360,7 +362,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
         for (int u = 0; u < U2; ++u) {
           const uint32_t i = i0 + u * HIST_B;
           if (i < m) {
-            atomicAdd(&h[digit_of(k[u], d)], 1u);
+            atomicAdd(&h[digit_w<DB>(k[u], d)], 1u);
             na[0] |= ~k[u].w0; o[0] |= k[u].w0;
             if constexpr (KW == 2) { na[1] |= ~k[u].w1; o[1] |= k[u].w1; }
             n_eq += (uint32_t)key_eq(k[u], probe);
@@ -370,15 +372,15 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
       }
     }
     __syncthreads();
-    for (int i = tid; i < RADIX; i += HIST_B) {
-      tile_pre[(size_t)t * RADIX + i] = run[i];
+    for (int i = tid; i < DG; i += HIST_B) {
+      tile_pre[(size_t)t * DG + i] = run[i];
       run[i] += h[i];
       h[i] = 0;
     }
     __syncthreads();
     cnt_recs += m;
   }
-  for (int i = tid; i < RADIX; i += HIST_B) ch_tot[(size_t)c * RADIX + i] = run[i];
+  for (int i = tid; i < DG; i += HIST_B) ch_tot[(size_t)c * DG + i] = run[i];
   if (tid == 0) ch_last[c] = cur;
   flush(cur);
   if (tid == 0 && cnt_recs) atomicAdd((unsigned long long*)&ctl->rec_hist, cnt_recs);
@@ -387,12 +389,13 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
 // -------------------------------------------------------------- k_carry
 // Carry of each chunk's first segment from the earlier chunks: a segmented
 // scan over the chunks, one thread per digit (single CTA; 32 chunks in flight).
-static __global__ void __launch_bounds__(RADIX) k_carry(const uint32_t* __restrict__ ch_first, const uint32_t* __restrict__ ch_last,
+template <int DG = RADIX>
+__global__ void __launch_bounds__(DG) k_carry(const uint32_t* __restrict__ ch_first, const uint32_t* __restrict__ ch_last,
                                                  const uint32_t* __restrict__ ch_tot, uint32_t nch,
                                                  uint32_t* __restrict__ carry_in) {
   const int d = threadIdx.x;
   uint32_t carry = 0, prev_last = NO_SEG;
-  constexpr int B = 32;
+  constexpr int B = DG > 256 ? 16 : 32;  // chunks in flight (1024 threads: 64 registers)
   for (uint32_t c0 = 0; c0 < nch; c0 += B) {
     uint32_t f[B], l[B], tt[B];
 #pragma unroll
@@ -400,14 +403,14 @@ static __global__ void __launch_bounds__(RADIX) k_carry(const uint32_t* __restri
       const uint32_t c = c0 + j;
       f[j] = c < nch ? __ldg(ch_first + c) : NO_SEG;
       l[j] = c < nch ? __ldg(ch_last + c) : NO_SEG;
-      tt[j] = c < nch ? __ldg(ch_tot + (size_t)c * RADIX + d) : 0u;
+      tt[j] = c < nch ? __ldg(ch_tot + (size_t)c * DG + d) : 0u;
     }
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const uint32_t c = c0 + j;
       if (c >= nch || f[j] == NO_SEG) continue;
       const uint32_t cin = (f[j] == prev_last) ? carry : 0u;
-      carry_in[(size_t)c * RADIX + d] = cin;
+      carry_in[(size_t)c * DG + d] = cin;
       carry = (f[j] == l[j] ? cin : 0u) + tt[j];
       prev_last = l[j];
     }
@@ -424,12 +427,12 @@ static __global__ void __launch_bounds__(RADIX) k_carry(const uint32_t* __restri
 // level with the few other keys of their bin ("bins with all keys
 // equal" generalised to "all but a few").  andor[s] holds 8
 // words: ~AND (2), OR (2), #keys == probe, #keys < probe (k_hist_pre).
-template <int R, int K>
-__global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict__ hist,
+template <int R, int K, int DG = RADIX>
+__global__ void __launch_bounds__(DG) k_plan(Seg* segs, uint32_t* __restrict__ hist,
                                                 const unsigned long long* __restrict__ andor,
                                                 uint32_t* __restrict__ segbase, Seg* large_next, Ctl* ctl,
                                                 uint32_t* __restrict__ splitc, int split_ok, int force = 0) {
-  __shared__ uint32_t ws[8];
+  __shared__ uint32_t ws[DG / 32];
   __shared__ int sh_const, sh_requeue;
   const uint32_t s = blockIdx.x;
   const int tid = threadIdx.x;
@@ -460,8 +463,9 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
         Seg ns = sg;
         ns.depth = (uint8_t)dt;
         ns.mode = MODE_NONE;
-        ns.flags = (uint8_t)(sg.flags & ~FLAG_CAND);
+        ns.flags = (uint8_t)(sg.flags & ~(FLAG_CAND | FLAG_SKIP_MASK));
         large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+        atomicAdd(&ctl->rec_large_next, (unsigned long long)sg.len);
         atomicMin(&ctl->d0, dt);
         sh_requeue = 1;
       }
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
   }
   __syncthreads();
   if (sh_requeue) return;
-  const uint32_t c = hist[(size_t)s * RADIX + tid];
+  const uint32_t c = hist[(size_t)s * DG + tid];
   if (c == sg.len && !force) sh_const = 1;
   __syncthreads();
   if (sh_const) {
@@ -485,7 +489,9 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
         Seg ns = sg;
         ns.depth = (uint8_t)d2;
         ns.mode = MODE_NONE;
+        ns.flags = (uint8_t)(sg.flags & ~FLAG_SKIP_MASK);
         large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+        atomicAdd(&ctl->rec_large_next, (unsigned long long)sg.len);
       }
     }
     return;
@@ -496,8 +502,8 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
   // and re-filled (records that are all key, R == K)
   if (split_ok && (sg.flags & FLAG_CAND) && 2ull * n_eq > sg.len && (sg.src == SRC_TMP || R == K)) {
     __syncthreads();
-    hist[(size_t)s * RADIX + tid] = tid == 0 ? n_lt : tid == 1 ? n_eq : tid == 2 ? sg.len - n_lt - n_eq : 0u;
-    if (tid < 3) segbase[(size_t)s * RADIX + tid] = sg.off + (tid >= 1 ? n_lt : 0u) + (tid == 2 ? n_eq : 0u);
+    hist[(size_t)s * DG + tid] = tid == 0 ? n_lt : tid == 1 ? n_eq : tid == 2 ? sg.len - n_lt - n_eq : 0u;
+    if (tid < 3) segbase[(size_t)s * DG + tid] = sg.off + (tid >= 1 ? n_lt : 0u) + (tid == 2 ? n_eq : 0u);
     if (tid < 4) splitc[(size_t)s * 4 + tid] = 0;
     if (tid == 0) {
       segs[s].mode = MODE_SPLIT;
@@ -506,8 +512,8 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
     }
     return;
   }
-  const uint32_t ex = block_excl_scan256(c, ws);
-  segbase[(size_t)s * RADIX + tid] = sg.off + ex;
+  const uint32_t ex = block_excl_scan<DG>(c, ws);
+  segbase[(size_t)s * DG + tid] = sg.off + ex;
   if (tid == 0) segs[s].mode = MODE_SCATTER;
 }
 
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(RADIX) k_plan(Seg* segs, uint32_t* __restrict_
 // tile twice from L1/L2 (the scatter's register prefetch of the tile warms
 // them) and is kept out of line so the digit scatter's register allocation
 // does not pay for it.  Every thread calls it.
-template <int R, int K, int SB>
+template <int R, int K, int SB, int DG = RADIX>
 __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base, uint32_t m, uint8_t* dst,
                                         uint8_t* recs, uint8_t* tmp, const uint32_t* __restrict__ segbase,
                                         uint32_t* __restrict__ splitc, uint8_t* stage, uint32_t* cnt,
@@ -551,7 +557,7 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
     if (q < m) rkv[q] = ((cl == 0u ? b0 : (cl == 1u ? b1 : b2)) + (uint32_t)__popc(mk & lanelt)) | (cl << 16);
   }
   __syncthreads();
-  if (tid < 3) gofs[tid] = segbase[(size_t)s * RADIX + tid] + atomicAdd(&splitc[(size_t)s * 4 + tid], cnt[tid]);
+  if (tid < 3) gofs[tid] = segbase[(size_t)s * DG + tid] + atomicAdd(&splitc[(size_t)s * 4 + tid], cnt[tid]);
   __syncthreads();
   const bool eq_skip = sg.src == SRC_REC;  // R == K: the equal run is filled later
   for (uint32_t q = tid; q < m; q += SB) {
@@ -570,7 +576,7 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
 constexpr int SCATTER_PAD = 64;  // dynamic smem beyond the TB-byte tile: the pad slot of absent records
 
-template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false>
+template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false, int DB = 8>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
@@ -584,9 +590,11 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   constexpr uint32_t T = tile_recs<R, TB, SB>();
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
+  constexpr int DG = 1 << DB;  // digits of the pass: 256, or 1024 on a wide level (one per thread)
+  static_assert(DG <= SB && (DB == 8 || (PRE && SB == DG)), "a wide pass: one thread per digit, reduce-then-scan offsets");
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
-  __shared__ uint32_t cnt[RADIX + 1], start[RADIX], gofs[RADIX], ws[8];  // cnt[RADIX]: absent records
+  __shared__ uint32_t cnt[DG + 1], start[DG], gofs[DG], ws[DG / 32];  // cnt[DG]: absent records
   __shared__ uint32_t sh_t, sh_s;
   const int tid = threadIdx.x;
   const uint32_t total = ctl->tiles_total;
@@ -615,12 +623,12 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     const Seg sg = segs[s];
     if (sg.mode != MODE_SCATTER && sg.mode != MODE_SPLIT) return;  // split tiles: a cache-warming prefetch
     if constexpr (PRE && R >= 16) {  // (R = 8 measured 0.5 % slower: registers)
-      if (sg.mode == MODE_SCATTER && tid < RADIX) {
+      if (sg.mode == MODE_SCATTER && tid < DG) {
         const uint32_t ch = t / per;
-        q_tp = __ldg(tile_pre + (size_t)t * RADIX + tid);
-        q_sb = __ldg(segbase + (size_t)s * RADIX + tid);
+        q_tp = __ldg(tile_pre + (size_t)t * DG + tid);
+        q_sb = __ldg(segbase + (size_t)s * DG + tid);
         q_cf = __ldg(ch_first + ch);
-        q_ci = __ldg(carry_in + (size_t)ch * RADIX + tid);
+        q_ci = __ldg(carry_in + (size_t)ch * DG + tid);
       }
     }
     const uint32_t lt = t - tile_start[s];
@@ -633,7 +641,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     }
   };
   if (tid == 0) take();
-  if (tid < RADIX) cnt[tid] = 0;
+  if (tid < DG) cnt[tid] = 0;
   __syncthreads();
   uint32_t t = sh_t, s = sh_s;
   if (t < total) load(t, s);
@@ -655,49 +663,49 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       uint32_t pre_excl = 0;
       if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry) + bin base, loaded with the tile
         if constexpr (R >= 16) {
-          if (tid < RADIX) pre_excl = q_tp + q_sb + (s == q_cf ? q_ci : 0u);
-        } else if (tid < RADIX) {
+          if (tid < DG) pre_excl = q_tp + q_sb + (s == q_cf ? q_ci : 0u);
+        } else if (tid < DG) {
           const uint32_t ch = t / per;
-          pre_excl = __ldg(tile_pre + (size_t)t * RADIX + tid) + __ldg(segbase + (size_t)s * RADIX + tid) +
-                     (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * RADIX + tid) : 0u);
+          pre_excl = __ldg(tile_pre + (size_t)t * DG + tid) + __ldg(segbase + (size_t)s * DG + tid) +
+                     (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * DG + tid) : 0u);
         }
       }
       uint32_t rk[(I + 1) / 2];  // ranks < T <= 2^16: two per register (fewer live registers under the cap)
 #pragma unroll
       for (int i = 0; i < (I + 1) / 2; ++i) rk[i] = 0;
-      // branch-free: an absent record (ragged last tile) counts in cnt[RADIX]
+      // branch-free: an absent record (ragged last tile) counts in cnt[DG]
       // and is staged in the pad slot T (no divergent branches around the atomics)
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
-        const uint32_t dg = idx < m ? digit_of(key_of<R, K>(r[i]), d) : (uint32_t)RADIX;
+        const uint32_t dg = idx < m ? digit_w<DB>(key_of<R, K>(r[i]), d) : (uint32_t)DG;
         rk[i >> 1] |= atomicAdd(&cnt[dg], 1u) << (16 * (i & 1));
       }
       __syncthreads();
       RS_PROF(1);
       uint32_t c = 0;
-      unsigned long long* my = status + (size_t)t * RADIX + tid;
-      if (tid < RADIX) {
+      unsigned long long* my = status + (size_t)t * DG + tid;
+      if (tid < DG) {
         c = cnt[tid];
         if constexpr (!PRE) st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
       }
       if (tid == 0) take();  // next ticket, ready before the stage barrier
-      const uint32_t ex = block_excl_scan256(c, ws);
-      if (tid < RADIX) start[tid] = ex;
+      const uint32_t ex = block_excl_scan<DG>(c, ws);
+      if (tid < DG) start[tid] = ex;
       __syncthreads();
       RS_PROF(2);
 #pragma unroll
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
-        const uint32_t pos = start[digit_of(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+        const uint32_t pos = start[digit_w<DB>(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
         st_rec<R>(stage + (size_t)(idx < m ? pos : T) * R, r[i]);
       }
       __syncthreads();  // r[] free, sh_t/sh_s hold the next ticket
       const uint32_t tn = sh_t, sn = sh_s;
-      if (tid < RADIX) cnt[tid] = 0;
+      if (tid < DG) cnt[tid] = 0;
       if (tn < total) load(tn, sn);
       RS_PROF(3);
-      if (tid < RADIX) {
+      if (tid < DG) {
         uint64_t excl = 0;
         if constexpr (PRE) {
           excl = pre_excl;  // includes the bin base
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
             unsigned long long w[LBW];
 #pragma unroll
             for (int j = 0; j < LBW; ++j)
-              w[j] = (p >= (uint32_t)j) ? ld_relaxed(status + (size_t)(p - j) * RADIX + tid) : 0ull;
+              w[j] = (p >= (uint32_t)j) ? ld_relaxed(status + (size_t)(p - j) * DG + tid) : 0ull;
             int j = 0;
             bool done = false;
 #pragma unroll
@@ -727,7 +735,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
           }
           st_relaxed(my, ep | ST_PREFIX | (excl + c));
         }
-        gofs[tid] = (PRE ? 0u : segbase[(size_t)s * RADIX + tid]) + (uint32_t)excl - ex;
+        gofs[tid] = (PRE ? 0u : segbase[(size_t)s * DG + tid]) + (uint32_t)excl - ex;
       }
       __syncthreads();
       RS_PROF(4);
@@ -742,14 +750,14 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
           if (h < 2 * m) v = reinterpret_cast<const uint4*>(stage)[h];
           Rec<16> hr;
           hr.a = v;
-          uint32_t dg = digit_of(key_of<16, K>(hr), d);
+          uint32_t dg = digit_w<DB>(key_of<16, K>(hr), d);
           dg = __shfl_sync(0xffffffffu, dg, lane & ~1);
           if (h < 2 * m) reinterpret_cast<uint4*>(dst + (size_t)(gofs[dg] + (h >> 1)) * R)[h & 1u] = v;
         }
       } else {
         for (uint32_t q = tid; q < m; q += SB) {
           const Rec<R> x = ld_rec<R>(stage + (size_t)q * R);
-          st_rec<R>(dst + (size_t)(gofs[digit_of(key_of<R, K>(x), d)] + q) * R, x);
+          st_rec<R>(dst + (size_t)(gofs[digit_w<DB>(key_of<R, K>(x), d)] + q) * R, x);
         }
       }
       moved += m;
@@ -764,10 +772,10 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       // final: written to `records` (segment in tmp), or skipped and filled
       // later (segment in `records`, R == K).
       if (tid == 0) take();  // next ticket (ordered before the barriers inside)
-      split_tile<R, K, SB>(sg, s, base, m, dst, recs, tmp, segbase, splitc, stage, cnt, gofs);
+      split_tile<R, K, SB, DG>(sg, s, base, m, dst, recs, tmp, segbase, splitc, stage, cnt, gofs);
       __syncthreads();  // sh_t/sh_s hold the next ticket; cnt / gofs / stage reusable
       const uint32_t tn = sh_t, sn = sh_s;
-      if (tid < RADIX) cnt[tid] = 0;
+      if (tid < DG) cnt[tid] = 0;
       if (tn < total) load(tn, sn);
       moved += m;
       t = tn;
@@ -814,16 +822,17 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
 // enumeration sort right here; <= TINY_MAX -> warp small-bin sorter right here
 // (§3.3); <= C -> Local list; larger -> next level's Large
 // list.  Dynamic smem: one TINY_MAX*R scratch per warp.
-template <int R, int K>
+template <int R, int K, int DB = 8>
 __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       const uint32_t* __restrict__ segbase, Seg* large_next,
                                                       Seg* local_cur, int cur, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
                                                       unsigned long long* __restrict__ probes, uint32_t lmin,
                                                       uint32_t lcap, uint32_t bitonic_max) {
   enum : uint8_t { C_NONE = 0, C_COPY = 1, C_ES = 2, C_TINY = 3 };
+  constexpr int DG = 1 << DB;  // children per segment (1024 on a wide level)
   extern __shared__ uint4 smem_raw[];
-  __shared__ uint8_t cls[RADIX];
-  __shared__ uint32_t coff[RADIX], clen[RADIX];
+  __shared__ uint8_t cls[DG];
+  __shared__ uint32_t coff[DG], clen[DG];
   __shared__ __align__(16) TailScratch<K> wsc[CHILD_B / 32];
   const uint32_t s = blockIdx.x;
   const Seg sg = segs[s];
@@ -835,12 +844,14 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
   const uint32_t d1 = split ? sg.depth : sg.depth + 1u;
   constexpr uint32_t C = local_capacity<R>();
   uint8_t* cbuf = buf_of(loc, recs, tmp);
-  if (tid < RADIX) {
-    const uint32_t len = hist[(size_t)s * RADIX + tid];
-    const uint32_t off = segbase[(size_t)s * RADIX + tid];
+  // children of a wide (10-bit) pass share the two leading bits of digit d1
+  const uint8_t cflags = (DB == 10 && !split) ? (uint8_t)(2u << FLAG_SKIP_SHIFT) : (uint8_t)0;
+  for (int v = tid; v < DG; v += CHILD_B) {
+    const uint32_t len = hist[(size_t)s * DG + v];
+    const uint32_t off = segbase[(size_t)s * DG + v];
     uint8_t c = C_NONE;
     if (len == 0) {
-    } else if (split && tid == 1) {  // the dominant key: final (written to records, or filled below)
+    } else if (split && v == 1) {  // the dominant key: final (written to records, or filled below)
       if (sg.src == SRC_REC) {
         const uint32_t pi = atomicAdd(&ctl->n_probe, 1u);
         const Key<K> pk = ld_key<R, K>(recs + (size_t)sg.off * R);  // untouched by the split scatter
@@ -868,24 +879,25 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
     } else if (len <= TINY_MAX) {
       c = C_TINY;
     } else if (len <= C || (len >= lmin && len <= lcap)) {  // CTA-local sort, or cluster-local sort in [lmin, lcap]
-      Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
+      Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, cflags, 0};
       local_cur[atomicAdd(&ctl->n_local[cur], 1u)] = ns;
       if (len <= small_cap<R>()) atomicAdd(&ctl->n_local_small[cur], 1u);
       else if (len <= med_cap<R>()) atomicAdd(&ctl->n_local_med[cur], 1u);
       atomicMax(&ctl->max_local_len[cur], len);
       atomicAdd(&ctl->bins_local, 1ull);
     } else {
-      Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, 0, 0};
+      Seg ns = {off, len, (uint8_t)d1, loc, MODE_NONE, cflags, 0};
       large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+      atomicAdd(&ctl->rec_large_next, (unsigned long long)len);
       atomicAdd(&ctl->bins_large, 1ull);
     }
-    cls[tid] = c;
-    coff[tid] = off;
-    clen[tid] = len;
+    cls[v] = c;
+    coff[v] = off;
+    clen[v] = len;
   }
   __syncthreads();
   unsigned long long tiny_recs = 0, tiny_bins = 0;
-  for (int v = warp; v < RADIX; v += CHILD_B / 32) {
+  for (int v = warp; v < DG; v += CHILD_B / 32) {
     const uint8_t c = cls[v];
     if (c == C_NONE) continue;
     const uint32_t off = coff[v], len = clen[v];
@@ -893,7 +905,7 @@ __global__ void __launch_bounds__(CHILD_B, 3) k_children(const Seg* __restrict__
     uint8_t* out = recs + (size_t)off * R;
     {  // the warp's next bin into L1 while this one is sorted (one 128-byte line per lane)
       const int vn = v + CHILD_B / 32;
-      if (vn < RADIX && (cls[vn] == C_TINY || cls[vn] == C_ES)) {
+      if (vn < DG && (cls[vn] == C_TINY || cls[vn] == C_ES)) {
         const uint8_t* pn = cbuf + (size_t)coff[vn] * R + (size_t)lane * 128;
         if ((uint32_t)lane * 128u < clen[vn] * (uint32_t)R) asm volatile("prefetch.global.L1 [%0];" ::"l"(pn));
       }
@@ -1214,6 +1226,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     constexpr bool BULK = LB >= 512;
     uint8_t* stg = BULK ? stage + ((uintptr_t)out & 15u) : stage;
     uint32_t d = sg.depth;
+    uint32_t sk = seg_skip(sg.flags);  // leading bits of digit d the bin already shares
     const uint32_t W = local_width(n, wmax);
     const uint32_t nbk = 1u << W;
     uint32_t rk[IP];
@@ -1234,7 +1247,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
           const uint32_t sh = 16u * (b & 1u);
           const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
           rk[i >> 1] |= old << (16 * (i & 1));
@@ -1281,6 +1294,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
       __syncthreads();
       if (d2 >= (uint32_t)K) { all_equal = true; break; }
       d = d2;
+      sk = 0;
     }
     const uint16_t* start16 = reinterpret_cast<const uint16_t*>(cnt);
     auto start_of = [&](uint32_t b) { return (uint32_t)start16[b]; };
@@ -1304,7 +1318,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
           const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
           st_rec<R>(stg + (size_t)(start_of(b) + rnk) * R, r[i]);
           if (rnk == 1u) blist[slot++] = b;
@@ -1323,18 +1337,20 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     prefetch_l2(nb + gridDim.x);
     bool tail = false;
     if (!all_equal) {
-      const bool fix = 8 * ((int)K - (int)d) > (int)W;  // key bits left below the composite digit
+      const bool fix = 8 * ((int)K - (int)d) - (int)sk > (int)W;  // key bits left below the composite digit
       RS_PROF(2);
       __syncthreads();  // staged
       RS_PROF(3);
       // the tail sorter's pivot path only in the small-bin configuration (duplicate-heavy
       // streams of small bins live there; the big-bin ones are short of registers)
       tail = local_finish<R, K, LB, NW, LB == 64>(stg, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
-                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl, BULK
+                                       reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl, BULK,
 #ifdef RADSORT_PHASE_PROF
-                                       , pfl
+                                       pfl,
+#else
+                                       nullptr,
 #endif
-      );
+                                       (int)(d + (sk + W) / 8u));
       pending = BULK;
     }
     done += n;
@@ -1728,7 +1744,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
 #pragma unroll
     for (int i = 0; i < IL; ++i) {
       if ((uint32_t)(i * LB + tid) < qn) {
-        const uint32_t b = bucket_of(key_of<R, K>(r[i]), g.depth, Wg), sh = 16u * (b & 1u);
+        const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * g.depth + seg_skip(g.flags), Wg), sh = 16u * (b & 1u);
         const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
         rk[i >> 1] |= old << (16 * (i & 1));
       }
@@ -1746,7 +1762,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
   cl.sync();  // #A: every CTA has counted
   bool pending = false;  // a bulk store still reads the stage
   while (bi < nlist) {
-    const uint32_t n = sg.len, d = sg.depth;
+    const uint32_t n = sg.len, d = sg.depth, sk = seg_skip(sg.flags);
     const uint32_t part = (n + CS - 1) / CS, p0 = min(n, crank * part), pn = min(n, p0 + part) - p0;
     const uint32_t W = max(local_width(n, wmax), WMIN);
     const uint32_t Wl = W - LCS, slice = 1u << Wl;
@@ -1835,12 +1851,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
       while (cm2) {
         const int q = __ffs(cm2) - 1;
         cm2 &= cm2 - 1u;
-        blist[b2++] = (c0 + j) * 8u + (uint32_t)q;
+        if (b2 < cap) blist[b2] = (c0 + j) * 8u + (uint32_t)q;  // (a longer list: the slice overflows
+        ++b2;                                                    // its stage, the bin is handed back)
       }
       while (cm3) {
         const int q = __ffs(cm3) - 1;
         cm3 &= cm3 - 1u;
-        blist[b3++] = (c0 + j) * 8u + (uint32_t)q;
+        if (b3 < cap) blist[b3] = (c0 + j) * 8u + (uint32_t)q;
+        ++b3;
       }
       uint4 run = o4;  // CTA k's records of a bucket follow those of CTAs < k
 #pragma unroll
@@ -1870,6 +1888,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
           Seg ns = sg;
           ns.mode = MODE_NONE;
           large_next[atomicAdd(&ctl->n_large_next, 1u)] = ns;
+          atomicAdd(&ctl->rec_large_next, (unsigned long long)ns.len);
         }
         __syncthreads();
         zero_cnt(2u << W);
@@ -1894,7 +1913,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if ((uint32_t)(i * LB + tid) < pn) {
-          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
           const uint32_t pos = (uint32_t)cnt16[b] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
           stg_rec<R>(bout + (size_t)(off[b >> Wl] + pos) * R, r[i]);
         }
@@ -1904,7 +1923,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if ((uint32_t)(i * LB + tid) < pn) {
-          const uint32_t b = bucket_of(key_of<R, K>(r[i]), d, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
           const uint32_t pos = (uint32_t)cnt16[b] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
           const uint32_t o = b >> Wl;
           st_rec<R>((o == crank ? stage : cl.map_shared_rank(stage, o)) + (size_t)pos * R, r[i]);
@@ -1927,7 +1946,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
     zero_cnt(2u << W);
     // 4. finish the slice (mixed buckets of > ES records go to the next Local
     // level: the tail sorter's scratch would alias the live counters)
-    const bool fix = 8 * ((int)K - (int)d) > (int)W;
+    const bool fix = 8 * ((int)K - (int)d) - (int)sk > (int)W;
     uint8_t* out = recs + ((size_t)sg.off + off[crank]) * R;
     if constexpr (DW) {  // the slice's colliding buckets, in place in global memory (L2-resident)
       global_fixup<R, K, LB>(out, reinterpret_cast<const uint16_t*>(sst), blist, mine, slice, d, W,
@@ -1936,11 +1955,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LB, 1)
       const bool bulk = mine && (((uintptr_t)out | ((uintptr_t)mine * R)) & 15u) == 0;
       local_finish<R, K, LB, NW, false, true>(stage, reinterpret_cast<const uint16_t*>(sst), blist, cap, mine, slice,
                                               d, W, fix ? s_np + s_n3 : 0u, &s_nbig, nullptr, out,
-                                              sg.off + off[crank], local_next, nxt, ctl, bulk
+                                              sg.off + off[crank], local_next, nxt, ctl, bulk,
 #ifdef RADSORT_PHASE_PROF
-                                              , pf + 4
+                                              pf + 4,
+#else
+                                              nullptr,
 #endif
-      );
+                                              (int)(d + (sk + W) / 8u));
       pending = bulk;
     }
     done += mine;

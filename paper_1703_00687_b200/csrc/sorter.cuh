@@ -403,6 +403,68 @@ struct Sorter {
     uint32_t nseg, depth;
   };
 
+  // One Large level: tile map, histogram + cross-tile prefix, plan, scatter,
+  // children.  DB = 8 (256 digits) or 10 (a wide level, 1024 digits; reduce-then-scan only).
+  template <uint32_t T_, int TB_, int SB_, int MINB_, int DB>
+  static radsort_status level_pass(Context* ctx, const Views& v, uint32_t n, uint32_t n_large, int cur, int nxt, uint8_t* recs,
+                         uint8_t* tmp, cudaStream_t st, Timer& tm, radsort_stats& stats, unsigned hist_grid, int occ_s,
+                         uint32_t* ch_first, uint32_t* ch_last, uint32_t* ch_tot, uint32_t* carry_in, bool cluster_ok,
+                         bool pre = true, int occ_h = 1) {
+    constexpr int DG = 1 << DB;
+    Seg* const* L = v.L;
+    Seg* const* Lo = v.Lo;
+    RS_CUDA(cudaMemsetAsync(v.hist, 0, (size_t)n_large * DG * sizeof(uint32_t), st));
+    RS_CUDA(cudaMemsetAsync(v.andor, 0, (size_t)n_large * 8 * sizeof(unsigned long long), st));
+    tm.begin(RADSORT_K_PLAN);
+    k_prep<<<1, 1024, 0, st>>>(L[cur], n_large, T_, v.tile_start, v.ctl, nxt);
+    const size_t tiles_ub = std::min(v.tiles_max, (size_t)n / T_ + n_large + 1);
+    k_tilemap<<<(unsigned)std::min<size_t>((tiles_ub + 255) / 256, (size_t)ctx->sms * 16), 256, 0, st>>>(
+        v.tile_start, n_large, v.ctl, v.tile_seg);
+    tm.end();
+    tm.begin(RADSORT_K_HIST);
+    if (pre) {
+      k_cand<R, K><<<(n_large + 7) / 8, 256, 0, st>>>(L[cur], n_large, recs, tmp);
+      k_hist_pre<R, K, T_, DB><<<hist_grid, HIST_B, 0, st>>>(L[cur], v.tile_start, n_large, v.ctl, v.hist, v.andor, recs,
+                                                            tmp, v.tile_pre, ch_first, ch_last, ch_tot, v.tile_seg);
+      k_carry<DG><<<1, DG, 0, st>>>(ch_first, ch_last, ch_tot, hist_grid, carry_in);
+    } else {
+      if constexpr (DB == 8) {
+        const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
+        k_hist<R, K, T_><<<gh, HIST_B, 0, st>>>(L[cur], v.tile_start, n_large, v.ctl, v.hist, v.andor, recs, tmp);
+      }
+    }
+    tm.end();
+    tm.begin(RADSORT_K_PLAN);
+    k_plan<R, K, DG><<<n_large, DG, 0, st>>>(L[cur], v.hist, v.andor, v.segbase, L[nxt], v.ctl, v.splitc, pre ? 1 : 0);
+    tm.end();
+    if (!pre && ++ctx->epoch >= 65536) {  // look-back status words are epoch-tagged, never cleared
+      RS_CUDA(cudaMemsetAsync(v.status, 0, ctx->status.bytes, st));
+      ctx->epoch = 1;
+    }
+    const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
+    tm.begin(RADSORT_K_SCATTER);
+    if (pre)
+      k_scatter<R, K, TB_, SB_, MINB_, true, false, DB><<<gs, SB_, TB_ + SCATTER_PAD, st>>>(
+          L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, v.tile_pre, ch_first,
+          carry_in, hist_grid, v.splitc, v.probes, v.tile_seg);
+    else if constexpr (DB == 8)
+      k_scatter<R, K, TB_, SB_, MINB_, false><<<gs, SB_, TB_ + SCATTER_PAD, st>>>(
+          L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, nullptr, nullptr, nullptr, 0,
+          v.splitc, v.probes, v.tile_seg);
+    tm.end();
+    tm.begin(RADSORT_K_CHILDREN);
+    k_children<R, K, DB><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(
+        L[cur], v.hist, v.segbase, L[nxt], Lo[cur], cur, v.ctl, recs, tmp, v.probes,
+        local_max() > C ? C + 1 : CL_MIN, local_max() > C ? local_max() : (cluster_ok ? ccap() : C), bitonic_max());
+    tm.end();
+    stats.kernel_launches[RADSORT_K_PLAN] += 2;
+    stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry
+    stats.kernel_launches[RADSORT_K_SCATTER]++;
+    stats.kernel_launches[RADSORT_K_CHILDREN]++;
+    stats.scatter_passes++;
+    return RADSORT_OK;
+  }
+
   static radsort_status run(Context* ctx, uint8_t* recs, uint8_t* tmp, uint32_t n, cudaStream_t st,
                             radsort_stats& stats, const Init* init = nullptr) {
     const char* e = getenv("RADSORT_SCATTER_CFG");
@@ -464,6 +526,28 @@ struct Sorter {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hist<R, K, T>, HIST_B, 0);
     occ_s = std::max(occ_s, 1);
     occ_h = std::max(occ_h, 1);
+    // wide levels (10-bit digit): 4x the tile (128 KiB), one 1024-thread CTA per SM, a thread per digit.
+    // RADSORT_WIDE=0 off, 1 the default rule, 2 forced wherever segments average >= 2 K records, 3 forced on
+    // every level (consecutive wide levels: segments sharing 2 bits of their digit; tests only)
+    // (built for the default 32 KiB x 256 tile configuration only)
+    constexpr bool WIDE_BUILT = TB == 32768 && SB == 256;
+    constexpr int TBW = 4 * TB, SBW = 1024;
+    constexpr uint32_t TW = tile_recs<R, TBW, SBW>();
+    static_assert(!WIDE_BUILT || TW == 4 * T, "a wide tile holds four 8-bit tiles (workspace sizing)");
+    const char* we = getenv("RADSORT_WIDE");
+    const int wide_mode = WIDE_BUILT ? (we ? atoi(we) : 1) : 0;
+    int occ_w = 1;
+    if constexpr (WIDE_BUILT) if (pre && wide_mode) {
+      smem_attr(ctx, k_scatter<R, K, TBW, SBW, 1, true, false, 10>, TBW + SCATTER_PAD);
+      smem_attr(ctx, k_children<R, K, 10>, CHILD_SCRATCH);
+      radsort_status rs2;
+      if ((rs2 = ensure(ctx->mlt, (size_t)hist_grid * 1024 * 4)) || (rs2 = ensure(ctx->mle, (size_t)hist_grid * 1024 * 4)))
+        return rs2;
+      ch_tot = (uint32_t*)ctx->mlt.p;
+      carry_in = (uint32_t*)ctx->mle.p;
+    }
+    bool prev_wide = false;
+    uint64_t level_recs = n;  // records of the level's Large list (the wide-level rule)
 
     Timer tm(ctx, st);
     const bool log = getenv("RADSORT_LOG") && getenv("RADSORT_LOG")[0] == '1';
@@ -489,6 +573,8 @@ struct Sorter {
       RS_CUDA(cudaMemcpyAsync(ctl, &c0, sizeof(Ctl), cudaMemcpyHostToDevice, st));
       RS_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
       n_large = (uint32_t)lg.size();
+      level_recs = 0;
+      for (const Seg& g : lg) level_recs += g.len;
     } else {
       k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
       n_large = n > C ? 1u : 0u;
@@ -512,54 +598,37 @@ struct Sorter {
       }
       const int nxt = cur ^ 1;
       if (n_large) {
-        RS_CUDA(cudaMemsetAsync(hist, 0, (size_t)n_large * RADIX * sizeof(uint32_t), st));
-        RS_CUDA(cudaMemsetAsync(andor, 0, (size_t)n_large * 8 * sizeof(unsigned long long), st));
-        tm.begin(RADSORT_K_PLAN);
-        k_prep<<<1, 1024, 0, st>>>(L[cur], n_large, T, tile_start, ctl, nxt);
-        const size_t tiles_ub = std::min(tiles_max, (size_t)n / T + n_large + 1);
-        k_tilemap<<<(unsigned)std::min<size_t>((tiles_ub + 255) / 256, (size_t)ctx->sms * 16), 256, 0, st>>>(
-            tile_start, n_large, ctl, v.tile_seg);
-        tm.end();
-        const unsigned gh = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_h);
-        tm.begin(RADSORT_K_HIST);
-        if (pre) {
-          k_cand<R, K><<<(n_large + 7) / 8, 256, 0, st>>>(L[cur], n_large, recs, tmp);
-          k_hist_pre<R, K, T><<<hist_grid, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp,
-                                                             tile_pre, ch_first, ch_last, ch_tot, v.tile_seg);
-          k_carry<<<1, RADIX, 0, st>>>(ch_first, ch_last, ch_tot, hist_grid, carry_in);
-        } else {
-          k_hist<R, K, T><<<gh, HIST_B, 0, st>>>(L[cur], tile_start, n_large, ctl, hist, andor, recs, tmp);
+        // wide level: one 10-bit pass instead of an 8-bit one where
+        // the 8-bit children would be too big for the CTA-local sort but the
+        // 10-bit ones fit it (saves a radix level / the cluster sort)
+        bool wide = false;
+        if (pre && wide_mode && (!prev_wide || wide_mode == 3)) {
+          const double avg = (double)level_recs / n_large;
+          wide = wide_mode == 3 ? avg >= 64.0
+                                : (wide_mode == 2 ? avg >= 2048.0 : (avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
         }
-        tm.end();
-        tm.begin(RADSORT_K_PLAN);
-        k_plan<R, K><<<n_large, RADIX, 0, st>>>(L[cur], hist, andor, segbase, L[nxt], ctl, v.splitc, pre ? 1 : 0);
-        tm.end();
-        if (!pre && ++ctx->epoch >= 65536) {  // look-back status words are epoch-tagged, never cleared
-          RS_CUDA(cudaMemsetAsync(status, 0, ctx->status.bytes, st));
-          ctx->epoch = 1;
+        if (wide) {  // the workspace is sized for 8-bit levels: grow it where a wide level needs more
+          // (between levels: the previous level's histograms, bases and tile prefixes are dead)
+          radsort_status rs2;
+          if ((rs2 = ensure(ctx->hist, (size_t)n_large * 1024 * 4)) || (rs2 = ensure(ctx->segbase, (size_t)n_large * 1024 * 4)) ||
+              (rs2 = ensure(ctx->tile_pre, ((size_t)n / TW + n_large + 1) * 1024 * 4)))
+            return rs2;
+          v.hist = (uint32_t*)ctx->hist.p;
+          v.segbase = (uint32_t*)ctx->segbase.p;
+          v.tile_pre = (uint32_t*)ctx->tile_pre.p;
         }
-        const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
-        tm.begin(RADSORT_K_SCATTER);
-        if (pre)
-          k_scatter<R, K, TB, SB, MINB, true><<<gs, SB, TB + SCATTER_PAD, st>>>(L[cur], tile_start, n_large, segbase, status,
-                                                                  ctx->epoch, ctl, recs, tmp, tile_pre, ch_first,
-                                                                  carry_in, hist_grid, v.splitc, v.probes, v.tile_seg);
-        else
-          k_scatter<R, K, TB, SB, MINB, false><<<gs, SB, TB + SCATTER_PAD, st>>>(L[cur], tile_start, n_large, segbase, status,
-                                                                   ctx->epoch, ctl, recs, tmp, nullptr, nullptr,
-                                                                   nullptr, 0, v.splitc, v.probes, v.tile_seg);
-        tm.end();
-        tm.begin(RADSORT_K_CHILDREN);
-        k_children<R, K><<<n_large, CHILD_B, CHILD_SCRATCH, st>>>(L[cur], hist, segbase, L[nxt], Lo[cur], cur, ctl, recs,
-                                                                  tmp, v.probes, local_max() > C ? C + 1 : CL_MIN,
-                                                                  local_max() > C ? local_max() : (cluster_ok ? ccap() : C),
-                                                                  bitonic_max());
-        tm.end();
-        stats.kernel_launches[RADSORT_K_PLAN] += 2;
-        stats.kernel_launches[RADSORT_K_HIST] += pre ? 2 : 1;  // k_hist_pre + k_carry
-        stats.kernel_launches[RADSORT_K_SCATTER]++;
-        stats.kernel_launches[RADSORT_K_CHILDREN]++;
-        stats.scatter_passes++;
+        radsort_status lrs = RADSORT_OK;
+        if constexpr (WIDE_BUILT) {
+          if (wide)
+            lrs = level_pass<TW, TBW, SBW, 1, 10>(ctx, v, n, n_large, cur, nxt, recs, tmp, st, tm, stats, hist_grid,
+                                                  occ_w, ch_first, ch_last, ch_tot, carry_in, cluster_ok);
+        }
+        if (!wide)
+          lrs = level_pass<T, TB, SB, MINB, 8>(ctx, v, n, n_large, cur, nxt, recs, tmp, st, tm, stats, hist_grid, occ_s,
+                                               ch_first, ch_last, ch_tot, carry_in, cluster_ok, pre, occ_h);
+        if (lrs) return lrs;
+        prev_wide = wide;
+        stats.wide_levels += wide ? 1 : 0;
       } else {
         k_prep<<<1, 1024, 0, st>>>(L[cur], 0, T, tile_start, ctl, nxt);
         stats.kernel_launches[RADSORT_K_PLAN]++;
@@ -571,8 +640,9 @@ struct Sorter {
       if (level == 0) stats.first_digit = c.d0;
       const uint32_t nloc = c.n_local[cur];
       if (log)
-        fprintf(stderr, "[radsort] level %d: large=%u tiles=%u -> large_next=%u local=%u (max %u)\n", level, n_large,
-                c.tiles_total, c.n_large_next, nloc, c.max_local_len[cur]);
+        fprintf(stderr, "[radsort] level %d%s: large=%u tiles=%u -> large_next=%u local=%u (max %u)\n", level,
+                prev_wide && n_large ? " (wide)" : "", n_large, c.tiles_total, c.n_large_next, nloc,
+                c.max_local_len[cur]);
       if (nloc) {
         tm.begin(RADSORT_K_LOCAL);
         int nl = 1;
@@ -585,6 +655,7 @@ struct Sorter {
           RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
           RS_CUDA(cudaStreamSynchronize(st));
           c.n_large_next = ctx->h_ctl->n_large_next;
+          c.rec_large_next = ctx->h_ctl->rec_large_next;
         }
       }
       stats.levels = level + 1;
@@ -601,6 +672,7 @@ struct Sorter {
       tm.flush(stats);
       if (c.n_large_next == 0 && nloc == 0 && n_large == 0) break;
       n_large = c.n_large_next;
+      level_recs = c.rec_large_next;
       cur = nxt;
     }
     // final statistics (one more small read; the sort's last kernels are ordered before it)
@@ -879,7 +951,7 @@ radsort_status multi_piece_hist(Context* ctx, PieceWs& w, const uint8_t* src, co
       dsegs, (const uint32_t*)w.tile_start.p, np, ctl, (uint32_t*)w.hist.p, (unsigned long long*)w.andor.p, src, src,
       (uint32_t*)w.tile_pre.p, (uint32_t*)w.ch_first.p, (uint32_t*)w.ch_last.p, (uint32_t*)w.ch_tot.p,
       (const uint32_t*)w.tile_seg.p);
-  k_carry<<<1, RADIX, 0, st>>>((const uint32_t*)w.ch_first.p, (const uint32_t*)w.ch_last.p,
+  k_carry<RADIX><<<1, RADIX, 0, st>>>((const uint32_t*)w.ch_first.p, (const uint32_t*)w.ch_last.p,
                                (const uint32_t*)w.ch_tot.p, w.hist_grid, (uint32_t*)w.carry_in.p);
   RS_CUDA(cudaGetLastError());
   RS_CUDA(cudaMemcpyAsync(h_hist, w.hist.p, (size_t)np * RADIX * 4, cudaMemcpyDeviceToHost, st));

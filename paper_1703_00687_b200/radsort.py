@@ -39,7 +39,7 @@ class Stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_uint32 * 8), ("kernel_ms", ctypes.c_float * 8),
         ("kernel_bytes", ctypes.c_uint64 * 8),
         ("bins_split", ctypes.c_uint64), ("records_split", ctypes.c_uint64),
-        ("exchange", ctypes.c_uint32), ("key_index", ctypes.c_uint32),
+        ("exchange", ctypes.c_uint32), ("key_index", ctypes.c_uint32), ("wide_levels", ctypes.c_uint32),
     ]
 
 

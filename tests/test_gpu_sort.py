@@ -430,3 +430,56 @@ def test_key_index_sort(R, K, ki, dist, monkeypatch):
         check(a, K)
         if n > C_of(R):
             assert rs.last_stats()["key_index"] == (1 if ki == "1" else 0)
+
+
+# ---- wide levels (10-bit digit: digit d + the two leading bits of digit d+1)
+def _wide_levels():
+    import paper_1703_00687_b200 as rs
+
+    return rs.last_stats()["wide_levels"]
+
+
+@pytest.mark.parametrize("R,K", LAYOUTS)
+@pytest.mark.parametrize("dist", ["uniform", "zipf", "sorted", "few", "consttop", "bytes", "uniform40"])
+def test_wide_level_forced(R, K, dist, monkeypatch):
+    # RADSORT_WIDE=2: every level whose segments average >= 2 K records scatters by 10 bits (the
+    # next level then by 8); sizes span several 1024-digit tiles, ragged tails, children of every
+    # class (tiny, local with the 2 shared bits, Large again)
+    monkeypatch.setenv("RADSORT_WIDE", "2")
+    payload = "index" if R > K else "random"
+    for n in (2_500, 300_001, 1_500_007):
+        a = dg.generate(n, R, K, dist, payload=payload, seed=4242 + n)
+        check(a, K)
+        if dist in ("uniform", "bytes") and n > C_of(R):
+            assert _wide_levels() >= 1, "no wide level ran"
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 16), (32, 16), (24, 8), (40, 16)])
+def test_wide_level_consecutive_and_split(R, K, monkeypatch):
+    # RADSORT_WIDE=3: every level wide, so wide levels also run on segments whose digit already
+    # shares two leading bits; and the dominant-key three-way split on a wide level
+    monkeypatch.setenv("RADSORT_WIDE", "3")
+    # uniform: level-0 children of ~1.3 C records are Large again -> a second wide level
+    for n, dist in ((int(1.3 * C_of(R) * 1024) + 7, "uniform"), (400_001, "zipf"), (200_003, "bytes")):
+        check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=99 + n), K)
+        assert _wide_levels() >= (2 if dist == "uniform" else 1)
+    monkeypatch.setenv("RADSORT_WIDE", "2")
+    a = dg.generate(1_000_003, R, K, "uniform", seed=98)
+    a[::3] = a[0]
+    a[1::3] = a[0]  # two thirds of the records carry one key: split three ways on the wide level 0
+    check(a, K)
+    assert _wide_levels() >= 1
+
+
+@pytest.mark.parametrize("R,K", [(32, 16), (32, 8)])
+def test_wide_level_default_rule(R, K, monkeypatch):
+    # the default rule takes a wide level where the 8-bit children would exceed the CTA-local
+    # capacity C and the 10-bit ones fit: segments averaging (256 C, 0.95 * 1024 C] records;
+    # one such segment at level 0 (n = 3.5 M for R = 32)
+    monkeypatch.delenv("RADSORT_WIDE", raising=False)
+    n = 3_500_000
+    check(dg.generate(n, R, K, "uniform", seed=7), K)
+    assert _wide_levels() == 1
+    monkeypatch.setenv("RADSORT_WIDE", "0")
+    check(dg.generate(n, R, K, "uniform", seed=7), K)
+    assert _wide_levels() == 0
