@@ -179,17 +179,28 @@ __device__ __forceinline__ uint32_t digit_of(const Key<16>& k, uint32_t d) {
   return d < 8 ? (uint32_t)(k.w1 >> (8u * (7u - d))) & 255u : (uint32_t)(k.w0 >> (8u * (15u - d))) & 255u;
 }
 
-// 1 <= W <= 32 key bits starting sb < 8K bits below the most significant one
-// (zero bits past the end of the key).
+// The 32 key bits starting sb < 8K bits below the most significant one (zero
+// bits past the end of the key): one funnel shift of the two 32-bit key words
+// that hold them (the word pair is selected by sb, uniform across a bin).
+__device__ __forceinline__ uint32_t key_window(const Key<8>& k, uint32_t sb) {
+  const uint32_t W0 = (uint32_t)(k.w0 >> 32), W1 = (uint32_t)k.w0;
+  const bool j0 = sb < 32;
+  return __funnelshift_l(j0 ? W1 : 0u, j0 ? W0 : W1, sb & 31u);
+}
+__device__ __forceinline__ uint32_t key_window(const Key<16>& k, uint32_t sb) {
+  const uint32_t W0 = (uint32_t)(k.w1 >> 32), W1 = (uint32_t)k.w1, W2 = (uint32_t)(k.w0 >> 32), W3 = (uint32_t)k.w0;
+  const uint32_t j = sb >> 5;
+  const uint32_t a = j == 0 ? W0 : (j == 1 ? W1 : (j == 2 ? W2 : W3));
+  const uint32_t b = j == 0 ? W1 : (j == 1 ? W2 : (j == 2 ? W3 : 0u));
+  return __funnelshift_l(b, a, sb & 31u);
+}
+// 1 <= W <= 32 key bits starting sb bits below the most significant one
+// (8-byte keys: one 64-bit shift pair, measured cheaper than the window).
 __device__ __forceinline__ uint32_t key_bits(const Key<8>& k, uint32_t sb, uint32_t W) {
   return (uint32_t)((k.w0 << sb) >> (64u - W));
 }
 __device__ __forceinline__ uint32_t key_bits(const Key<16>& k, uint32_t sb, uint32_t W) {
-  uint64_t x;
-  if (sb == 0) x = k.w1;
-  else if (sb < 64) x = (k.w1 << sb) | (k.w0 >> (64u - sb));
-  else x = k.w0 << (sb - 64u);
-  return (uint32_t)(x >> (64u - W));
+  return key_window(k, sb) >> (32u - W);
 }
 // The radix digit of a pass of DB bits at depth d: DB = 8 is digit d (one key
 // byte); DB = 10 is digit d followed by the two leading bits of
@@ -197,7 +208,7 @@ __device__ __forceinline__ uint32_t key_bits(const Key<16>& k, uint32_t sb, uint
 template <int DB, int K>
 __device__ __forceinline__ uint32_t digit_w(const Key<K>& k, uint32_t d) {
   if constexpr (DB == 8) return digit_of(k, d);
-  else return key_bits(k, 8u * d, (uint32_t)DB);
+  else return key_window(k, 8u * d) >> (32 - DB);
 }
 
 // First digit >= d whose byte differs between the AND and the OR of all keys

@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(LB, 1)
     const int lim = (int)n - tid;
     uint8_t* out = recs + (size_t)sg.off * R;
     uint8_t* stg = stage + ((uintptr_t)out & 15u);
-    uint32_t d = sg.depth;
-    uint32_t sk = seg_skip(sg.flags);  // leading bits of digit d the bin already shares
+    // key bits the bin's records already share (digits, plus 2 bits below a wide level)
+    uint32_t sb = 8u * sg.depth + seg_skip(sg.flags);
     const uint32_t W = (uint32_t)max((int)LOCAL_WMIN, min((int)wmax, (int)local_width(n, wmax) + wdelta));
     const uint32_t nbk = 1u << W;
     uint32_t rk[IP];
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(LB, 1)
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), sb, W);
           const uint32_t sh = 16u * (b & 1u);
           const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
           rk[i >> 1] |= old << (16 * (i & 1));
@@ -213,19 +213,18 @@ __global__ void __launch_bounds__(LB, 1)
       }
       __syncthreads();
       uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
-      const uint32_t d2 = first_nonconst_digit<K>(A, O, d);
+      const uint32_t d2 = first_nonconst_digit<K>(A, O, sb / 8u);
       __syncthreads();
       zero_cnt(2u << W);
       if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
       if (tid == 0) s_const = 0;
       __syncthreads();
       if (d2 >= (uint32_t)K) { all_equal = true; break; }
-      d = d2;
-      sk = 0;
+      sb = 8u * d2;
     }
     const uint32_t q = par ^ 1u;  // this bin's list parity
     const uint16_t* start16 = reinterpret_cast<const uint16_t*>(cnt);
-    const bool fix = 8 * ((int)K - (int)d) - (int)sk > (int)W;  // key bits left below the composite digit
+    const bool fix = 8u * K > sb + W;  // key bits left below the composite digit
     if (all_equal) {  // final where it is (copied out of tmp)
       if (sg.src == SRC_TMP) {
 #pragma unroll
@@ -245,7 +244,7 @@ __global__ void __launch_bounds__(LB, 1)
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), sb, W);
           const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
           st_rec<R>(stg + (size_t)(start16[b] + rnk) * R, r[i]);
           if (rnk == 1u && fix) blist[slot++] = b;  // the bucket; turned into start | count below
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(LB, 1)
       p_n = n;
       p_ncol = s_ncol[q];
       p_off = sg.off;
-      p_nd = d + (sk + W) / 8u;  // digits shared by a bucket's keys
+      p_nd = (sb + W) / 8u;  // digits shared by a bucket's keys
       // collision list: bucket -> start | count << 16 (the counters are reused by the next bin)
       for (uint32_t e = tid; e < p_ncol; e += LB) {
         const uint32_t b = blist[e], s0 = start16[b];

@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(HIST_B, 4) k_hist_pre(const Seg* __restrict__ 
                                                      uint32_t* __restrict__ ch_tot, const uint32_t* __restrict__ tile_seg) {
   constexpr int KW = K / 8;
   constexpr int DG = 1 << DB;  // digits of the pass (256, or 1024 on a wide level)
-  constexpr int U = R <= 8 ? 16 : 8;  // keys in flight per thread
+  constexpr int U = DB == 10 ? (R <= 8 ? 8 : 4) : (R <= 8 ? 16 : 8);  // keys in flight per thread (wide: registers)
   __shared__ uint32_t h[DG], run[DG];
   __shared__ unsigned long long sna[2], so[2];
   const uint32_t total = ctl->tiles_total;
@@ -1225,8 +1225,8 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     // c2 1.82 vs 1.86, kmc 12.9 vs 14.3 ms)
     constexpr bool BULK = LB >= 512;
     uint8_t* stg = BULK ? stage + ((uintptr_t)out & 15u) : stage;
-    uint32_t d = sg.depth;
-    uint32_t sk = seg_skip(sg.flags);  // leading bits of digit d the bin already shares
+    // key bits the bin's records already share (digits, plus 2 bits below a wide level)
+    uint32_t sb = 8u * sg.depth + seg_skip(sg.flags);
     const uint32_t W = local_width(n, wmax);
     const uint32_t nbk = 1u << W;
     uint32_t rk[IP];
@@ -1247,7 +1247,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), sb, W);
           const uint32_t sh = 16u * (b & 1u);
           const uint32_t old = (atomicAdd(&cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
           rk[i >> 1] |= old << (16 * (i & 1));
@@ -1286,15 +1286,14 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
       }
       __syncthreads();
       uint64_t A[2] = {~(uint64_t)sna[0], ~(uint64_t)sna[1]}, O[2] = {so[0], so[1]};
-      const uint32_t d2 = first_nonconst_digit<K>(A, O, d);
+      const uint32_t d2 = first_nonconst_digit<K>(A, O, sb / 8u);
       __syncthreads();
       zero_cnt(2u << W);
       if (tid < 2) { sna[tid] = 0; so[tid] = 0; }
       if (tid == 0) s_const = 0;
       __syncthreads();
       if (d2 >= (uint32_t)K) { all_equal = true; break; }
-      d = d2;
-      sk = 0;
+      sb = 8u * d2;
     }
     const uint16_t* start16 = reinterpret_cast<const uint16_t*>(cnt);
     auto start_of = [&](uint32_t b) { return (uint32_t)start16[b]; };
@@ -1318,7 +1317,7 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 #pragma unroll
       for (int i = 0; i < IL; ++i) {
         if (i * LB < lim) {
-          const uint32_t b = key_bits(key_of<R, K>(r[i]), 8u * d + sk, W);
+          const uint32_t b = key_bits(key_of<R, K>(r[i]), sb, W);
           const uint32_t rnk = (rk[i >> 1] >> (16 * (i & 1))) & 0xffffu;
           st_rec<R>(stg + (size_t)(start_of(b) + rnk) * R, r[i]);
           if (rnk == 1u) blist[slot++] = b;
@@ -1337,20 +1336,20 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
     prefetch_l2(nb + gridDim.x);
     bool tail = false;
     if (!all_equal) {
-      const bool fix = 8 * ((int)K - (int)d) - (int)sk > (int)W;  // key bits left below the composite digit
+      const bool fix = 8u * K > sb + W;  // key bits left below the composite digit
       RS_PROF(2);
       __syncthreads();  // staged
       RS_PROF(3);
       // the tail sorter's pivot path only in the small-bin configuration (duplicate-heavy
       // streams of small bins live there; the big-bin ones are short of registers)
-      tail = local_finish<R, K, LB, NW, LB == 64>(stg, start16, blist, cap, n, nbk, d, W, fix ? s_ncol : 0u, &s_nbig,
+      tail = local_finish<R, K, LB, NW, LB == 64>(stg, start16, blist, cap, n, nbk, sb / 8u, W, fix ? s_ncol : 0u, &s_nbig,
                                        reinterpret_cast<TailScratch<K>*>(cnt), out, sg.off, local_next, nxt, ctl, BULK,
 #ifdef RADSORT_PHASE_PROF
                                        pfl,
 #else
                                        nullptr,
 #endif
-                                       (int)(d + (sk + W) / 8u));
+                                       (int)((sb + W) / 8u));
       pending = BULK;
     }
     done += n;
