@@ -576,7 +576,7 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
 constexpr int SCATTER_PAD = 64;  // dynamic smem beyond the TB-byte tile: the pad slot of absent records
 
-template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false, int DB = 8>
+template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false, int DB = 8, bool TMA_OUT = false>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
@@ -590,11 +590,17 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   constexpr uint32_t T = tile_recs<R, TB, SB>();
   constexpr int I = (int)(T / SB);
   constexpr int LBW = 8;  // look-back window: predecessor statuses loaded in parallel
-  constexpr int DG = 1 << DB;  // digits of the pass: 256, or 1024 on a wide level (one per thread)
-  static_assert(DG <= SB && (DB == 8 || (PRE && SB == DG)), "a wide pass: one thread per digit, reduce-then-scan offsets");
+  constexpr int DG = 1 << DB;  // digits of the pass: 256, or 1024 on a wide level
+  constexpr int DPT = DG > SB ? DG / SB : 1;  // digits per thread (consecutive: tid * DPT + j)
+  static_assert(DB == 8 ? DG <= SB : (PRE && (SB == DG || 2 * SB == DG)),
+                "a wide pass: one or two digits per thread, reduce-then-scan offsets");
+  // TMA write-out: every digit's staged run leaves as one bulk copy (cp.async.bulk
+  // shared -> global, issued by the digit's thread) that drains while the next
+  // tile is loaded, ranked and scanned; needs 16-byte aligned runs (R = 16, 32)
+  constexpr bool TW = TMA_OUT && PRE && !PEER && (R == 16 || R == 32);
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
-  __shared__ uint32_t cnt[DG + 1], start[DG], gofs[DG], ws[DG / 32];  // cnt[DG]: absent records
+  __shared__ uint32_t cnt[DG + 1], start[DG], gofs[DG], ws[(DPT == 1 ? DG : SB) / 32];  // cnt[DG]: absent records
   __shared__ uint32_t sh_t, sh_s;
   const int tid = threadIdx.x;
   const uint32_t total = ctl->tiles_total;
@@ -615,7 +621,8 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   Rec<R> r[I];
   // reduce-then-scan offsets of the loaded tile (PRE), loaded with its records
   // and summed only when the tile is processed, so no warp waits on them
-  uint32_t q_tp = 0, q_sb = 0, q_cf = 0, q_ci = 0;
+  uint32_t q_tp[DPT] = {}, q_sb[DPT] = {}, q_cf = 0, q_ci[DPT] = {};
+  const bool has_dg = tid * DPT < DG;  // this thread owns digits tid * DPT ..
   const uint32_t per = PRE ? (total + hist_grid - 1) / hist_grid : 1u;
   // issue this tile's loads into r[] (software pipelining: the loads of tile
   // k+1 are in flight while tile k is looked back and written out)
@@ -623,12 +630,16 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     const Seg sg = segs[s];
     if (sg.mode != MODE_SCATTER && sg.mode != MODE_SPLIT) return;  // split tiles: a cache-warming prefetch
     if constexpr (PRE && R >= 16) {  // (R = 8 measured 0.5 % slower: registers)
-      if (sg.mode == MODE_SCATTER && tid < DG) {
+      if (sg.mode == MODE_SCATTER && has_dg) {
         const uint32_t ch = t / per;
-        q_tp = __ldg(tile_pre + (size_t)t * DG + tid);
-        q_sb = __ldg(segbase + (size_t)s * DG + tid);
         q_cf = __ldg(ch_first + ch);
-        q_ci = __ldg(carry_in + (size_t)ch * DG + tid);
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {
+          const uint32_t v = (uint32_t)(tid * DPT + j);
+          q_tp[j] = __ldg(tile_pre + (size_t)t * DG + v);
+          q_sb[j] = __ldg(segbase + (size_t)s * DG + v);
+          q_ci[j] = __ldg(carry_in + (size_t)ch * DG + v);
+        }
       }
     }
     const uint32_t lt = t - tile_start[s];
@@ -641,7 +652,9 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     }
   };
   if (tid == 0) take();
-  if (tid < DG) cnt[tid] = 0;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j)
+    if (tid * DPT + j < DG) cnt[tid * DPT + j] = 0;
   __syncthreads();
   uint32_t t = sh_t, s = sh_s;
   if (t < total) load(t, s);
@@ -660,14 +673,22 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
                         : buf_of(sg.src == SRC_TMP ? SRC_REC : SRC_TMP, recs, tmp);
     if (sg.mode == MODE_SCATTER) {
       const uint32_t d = sg.depth;
-      uint32_t pre_excl = 0;
+      uint32_t pre_excl[DPT] = {};
       if constexpr (PRE) {  // reduce-then-scan offsets (k_hist_pre / k_carry) + bin base, loaded with the tile
         if constexpr (R >= 16) {
-          if (tid < DG) pre_excl = q_tp + q_sb + (s == q_cf ? q_ci : 0u);
-        } else if (tid < DG) {
+          if (has_dg) {
+#pragma unroll
+            for (int j = 0; j < DPT; ++j) pre_excl[j] = q_tp[j] + q_sb[j] + (s == q_cf ? q_ci[j] : 0u);
+          }
+        } else if (has_dg) {
           const uint32_t ch = t / per;
-          pre_excl = __ldg(tile_pre + (size_t)t * DG + tid) + __ldg(segbase + (size_t)s * DG + tid) +
-                     (s == __ldg(ch_first + ch) ? __ldg(carry_in + (size_t)ch * DG + tid) : 0u);
+          const bool first = s == __ldg(ch_first + ch);
+#pragma unroll
+          for (int j = 0; j < DPT; ++j) {
+            const uint32_t v = (uint32_t)(tid * DPT + j);
+            pre_excl[j] = __ldg(tile_pre + (size_t)t * DG + v) + __ldg(segbase + (size_t)s * DG + v) +
+                          (first ? __ldg(carry_in + (size_t)ch * DG + v) : 0u);
+          }
         }
       }
       uint32_t rk[(I + 1) / 2];  // ranks < T <= 2^16: two per register (fewer live registers under the cap)
@@ -683,15 +704,26 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       }
       __syncthreads();
       RS_PROF(1);
-      uint32_t c = 0;
+      uint32_t c[DPT] = {};
       unsigned long long* my = status + (size_t)t * DG + tid;
-      if (tid < DG) {
-        c = cnt[tid];
-        if constexpr (!PRE) st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c);
+      if (has_dg) {
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) c[j] = cnt[tid * DPT + j];
+        if constexpr (!PRE) st_relaxed(my, ep | (lt == 0 ? ST_PREFIX : ST_AGG) | c[0]);
       }
       if (tid == 0) take();  // next ticket, ready before the stage barrier
-      const uint32_t ex = block_excl_scan<DG>(c, ws);
-      if (tid < DG) start[tid] = ex;
+      uint32_t ex[DPT];
+      if constexpr (DPT == 1) {
+        ex[0] = block_excl_scan<DG>(c[0], ws);
+      } else {
+        ex[0] = block_excl_scan<SB>(c[0] + c[1], ws);
+        ex[1] = ex[0] + c[0];
+      }
+      if (has_dg) {
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) start[tid * DPT + j] = ex[j];
+      }
+      if constexpr (TW) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the stage is free
       __syncthreads();
       RS_PROF(2);
 #pragma unroll
@@ -700,15 +732,37 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
         const uint32_t pos = start[digit_w<DB>(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
         st_rec<R>(stage + (size_t)(idx < m ? pos : T) * R, r[i]);
       }
+      if constexpr (TW) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staged -> visible to TMA
       __syncthreads();  // r[] free, sh_t/sh_s hold the next ticket
       const uint32_t tn = sh_t, sn = sh_s;
-      if (tid < DG) cnt[tid] = 0;
+#pragma unroll
+      for (int j = 0; j < DPT; ++j)
+        if (tid * DPT + j < DG) cnt[tid * DPT + j] = 0;
       if (tn < total) load(tn, sn);
       RS_PROF(3);
-      if (tid < DG) {
+      if constexpr (TW) {
+        if (has_dg) {
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < DPT; ++j) {
+            if (c[j]) {
+              const uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + (size_t)ex[j] * R);
+              uint8_t* ga = dst + (size_t)pre_excl[j] * R;
+              asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(ga), "r"(sa),
+                           "r"(c[j] * (uint32_t)R)
+                           : "memory");
+              any = true;
+            }
+          }
+          if (any) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else if constexpr (DPT == 2) {
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) gofs[tid * DPT + j] = pre_excl[j] - ex[j];
+      } else if (has_dg) {
         uint64_t excl = 0;
         if constexpr (PRE) {
-          excl = pre_excl;  // includes the bin base
+          excl = pre_excl[0];  // includes the bin base
         } else if (lt > 0) {
           // windowed decoupled look-back over this segment's earlier tiles
           uint32_t p = t - 1;
@@ -733,13 +787,14 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
             if (tid == 0) pf[6]++;
 #endif
           }
-          st_relaxed(my, ep | ST_PREFIX | (excl + c));
+          st_relaxed(my, ep | ST_PREFIX | (excl + c[0]));
         }
-        gofs[tid] = (PRE ? 0u : segbase[(size_t)s * DG + tid]) + (uint32_t)excl - ex;
+        gofs[tid] = (PRE ? 0u : segbase[(size_t)s * DG + tid]) + (uint32_t)excl - ex[0];
       }
-      __syncthreads();
+      if constexpr (!TW) __syncthreads();
       RS_PROF(4);
-      if constexpr (R == 32) {
+      if constexpr (TW) {
+      } else if constexpr (R == 32) {
         // a lane pair moves one record, 16 bytes each: consecutive 16-byte smem
         // reads (a lane per 32-byte record conflicts 2-way on every read); the
         // key sits in the first half, its digit is passed to the partner lane
@@ -772,10 +827,16 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       // final: written to `records` (segment in tmp), or skipped and filled
       // later (segment in `records`, R == K).
       if (tid == 0) take();  // next ticket (ordered before the barriers inside)
+      if constexpr (TW) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+      }
       split_tile<R, K, SB, DG>(sg, s, base, m, dst, recs, tmp, segbase, splitc, stage, cnt, gofs);
       __syncthreads();  // sh_t/sh_s hold the next ticket; cnt / gofs / stage reusable
       const uint32_t tn = sh_t, sn = sh_s;
-      if (tid < DG) cnt[tid] = 0;
+#pragma unroll
+      for (int j = 0; j < DPT; ++j)
+        if (tid * DPT + j < DG) cnt[tid * DPT + j] = 0;
       if (tn < total) load(tn, sn);
       moved += m;
       t = tn;
@@ -806,6 +867,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
     RS_PROF(5);
   }
   if constexpr (PEER) __threadfence_system();  // peer stores performed before the kernel's completion is observed
+  if constexpr (TW) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (tid == 0 && moved) atomicAdd(&ctl->rec_scatter, moved);
 #ifdef RADSORT_PHASE_PROF
   if (tid == 0) {

@@ -403,6 +403,13 @@ struct Sorter {
     uint32_t nseg, depth;
   };
 
+  // the scatter's digit runs leave by TMA bulk copies (R = 16, 32; RADSORT_SCATTER_TMA=0: thread stores;
+  // c4 level-0 scatter 11.8 -> 10.3 ms, c2 2.39 -> 2.16 ms)
+  static bool scatter_tma() {
+    const char* e = getenv("RADSORT_SCATTER_TMA");
+    return (R == 16 || R == 32) && !(e && e[0] == '0');
+  }
+
   // One Large level: tile map, histogram + cross-tile prefix, plan, scatter,
   // children.  DB = 8 (256 digits) or 10 (a wide level, 1024 digits; reduce-then-scan only).
   template <uint32_t T_, int TB_, int SB_, int MINB_, int DB>
@@ -443,7 +450,13 @@ struct Sorter {
     }
     const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
     tm.begin(RADSORT_K_SCATTER);
-    if (pre)
+    if (pre && scatter_tma()) {
+      auto* kfn = k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true>;
+      smem_attr(ctx, kfn, TB_ + SCATTER_PAD);
+      kfn<<<gs, SB_, TB_ + SCATTER_PAD, st>>>(L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs,
+                                              tmp, v.tile_pre, ch_first, carry_in, hist_grid, v.splitc, v.probes,
+                                              v.tile_seg, nullptr);
+    } else if (pre)
       k_scatter<R, K, TB_, SB_, MINB_, true, false, DB><<<gs, SB_, TB_ + SCATTER_PAD, st>>>(
           L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, v.tile_pre, ch_first,
           carry_in, hist_grid, v.splitc, v.probes, v.tile_seg);
@@ -531,14 +544,17 @@ struct Sorter {
     // every level (consecutive wide levels: segments sharing 2 bits of their digit; tests only)
     // (built for the default 32 KiB x 256 tile configuration only)
     constexpr bool WIDE_BUILT = TB == 32768 && SB == 256;
-    constexpr int TBW = 4 * TB, SBW = 1024;
-    constexpr uint32_t TW = tile_recs<R, TBW, SBW>();
-    static_assert(!WIDE_BUILT || TW == 4 * T, "a wide tile holds four 8-bit tiles (workspace sizing)");
+    constexpr int TBW = 4 * TB, SBW = 1024;  // RADSORT_WIDE_CFG=1: one 1024-thread CTA per SM, a digit per thread
+    constexpr int TBW2 = 2 * TB, SBW2 = 512;  // (default) two 512-thread CTAs per SM, two digits per thread
+    constexpr uint32_t TW = tile_recs<R, TBW, SBW>(), TW2 = tile_recs<R, TBW2, SBW2>();
+    const char* wc = getenv("RADSORT_WIDE_CFG");
+    const int wide_cfg = wc ? atoi(wc) : 2;  // measured: c4 wide scatter 13.75 (1) vs 13.13 ms (2)
     const char* we = getenv("RADSORT_WIDE");
     const int wide_mode = WIDE_BUILT ? (we ? atoi(we) : 1) : 0;
     int occ_w = 1;
     if constexpr (WIDE_BUILT) if (pre && wide_mode) {
       smem_attr(ctx, k_scatter<R, K, TBW, SBW, 1, true, false, 10>, TBW + SCATTER_PAD);
+      smem_attr(ctx, k_scatter<R, K, TBW2, SBW2, 2, true, false, 10>, TBW2 + SCATTER_PAD);
       smem_attr(ctx, k_children<R, K, 10>, CHILD_SCRATCH);
       radsort_status rs2;
       if ((rs2 = ensure(ctx->mlt, (size_t)hist_grid * 1024 * 4)) || (rs2 = ensure(ctx->mle, (size_t)hist_grid * 1024 * 4)))
@@ -611,7 +627,7 @@ struct Sorter {
           // (between levels: the previous level's histograms, bases and tile prefixes are dead)
           radsort_status rs2;
           if ((rs2 = ensure(ctx->hist, (size_t)n_large * 1024 * 4)) || (rs2 = ensure(ctx->segbase, (size_t)n_large * 1024 * 4)) ||
-              (rs2 = ensure(ctx->tile_pre, ((size_t)n / TW + n_large + 1) * 1024 * 4)))
+              (rs2 = ensure(ctx->tile_pre, ((size_t)n / std::min(TW, TW2) + n_large + 1) * 1024 * 4)))
             return rs2;
           v.hist = (uint32_t*)ctx->hist.p;
           v.segbase = (uint32_t*)ctx->segbase.p;
@@ -619,7 +635,10 @@ struct Sorter {
         }
         radsort_status lrs = RADSORT_OK;
         if constexpr (WIDE_BUILT) {
-          if (wide)
+          if (wide && wide_cfg == 2)
+            lrs = level_pass<TW2, TBW2, SBW2, 2, 10>(ctx, v, n, n_large, cur, nxt, recs, tmp, st, tm, stats, hist_grid,
+                                                     2, ch_first, ch_last, ch_tot, carry_in, cluster_ok);
+          else if (wide)
             lrs = level_pass<TW, TBW, SBW, 1, 10>(ctx, v, n, n_large, cur, nxt, recs, tmp, st, tm, stats, hist_grid,
                                                   occ_w, ch_first, ch_last, ch_tot, carry_in, cluster_ok);
         }
