@@ -616,12 +616,16 @@ struct Sorter {
       if (n_large) {
         // wide level: one 10-bit pass instead of an 8-bit one where
         // the 8-bit children would be too big for the CTA-local sort but the
-        // 10-bit ones fit it (saves a radix level / the cluster sort)
+        // 10-bit ones fit it (saves a radix level / the cluster sort).  Default for
+        // R >= 24 only: for R = 8 / 16 the 10-bit pass costs more than it saves
+        // (c5 16.6 -> 17.5, c2 5.3 -> 5.9 ms) and duplicate-heavy bins near C make
+        // the local sort slow (kmc 27.8 -> 55.6 ms; measured)
         bool wide = false;
         if (pre && wide_mode && (!prev_wide || wide_mode == 3)) {
           const double avg = (double)level_recs / n_large;
           wide = wide_mode == 3 ? avg >= 64.0
-                                : (wide_mode == 2 ? avg >= 2048.0 : (avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
+                                : (wide_mode == 2 ? avg >= 2048.0
+                                                  : (R >= 24 && avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
         }
         if (wide) {  // the workspace is sized for 8-bit levels: grow it where a wide level needs more
           // (between levels: the previous level's histograms, bases and tile prefixes are dead)

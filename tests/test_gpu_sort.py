@@ -475,7 +475,7 @@ def test_wide_level_consecutive_and_split(R, K, monkeypatch):
 def test_wide_level_default_rule(R, K, monkeypatch):
     # the default rule takes a wide level where the 8-bit children would exceed the CTA-local
     # capacity C and the 10-bit ones fit: segments averaging (256 C, 0.95 * 1024 C] records;
-    # one such segment at level 0 (n = 3.5 M for R = 32)
+    # one such segment at level 0 (n = 3.5 M for R = 32); default for R >= 24 only
     monkeypatch.delenv("RADSORT_WIDE", raising=False)
     n = 3_500_000
     check(dg.generate(n, R, K, "uniform", seed=7), K)
