@@ -342,6 +342,8 @@ def run_radsort(args):
         ach = b / (ms / 1e3) / 1e9
         nl = max(1, launches_per_step.get(k, 1))
         tr = traffic_map.get(k)
+        if tr is not None and traffic_map.get("_per") == "step":  # bytes per sort -> per launch, as `achieved`
+            tr = round(tr / nl)
         roof_all[k] = {"bound": "hbm", "kernel": names[k], "achieved": round(ach, 1), "peak": peak,
                        "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
                        "traffic": tr, "bytes_per_launch": b / args.steps / nl, "launches_per_step": nl,

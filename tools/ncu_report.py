@@ -5,6 +5,7 @@ ncu_traffic / launch_summary scripts).
     python tools/ncu_report.py launches LAUNCHES.csv        # --metrics launch list: time, share, DRAM per kernel
     python tools/ncu_report.py full REP.ncu-rep [--lines N]  # --set full capture: key counters, stalls, hot lines
     python tools/ncu_report.py traffic REP.ncu-rep [local=N] # DRAM bytes per launch by kernel family (JSON)
+    python tools/ncu_report.py steptraffic LAUNCHES.csv SORTS  # DRAM bytes per sort by kernel class (JSON, bench.py)
 """
 import collections
 import csv
@@ -116,12 +117,38 @@ def traffic(rep, phase):
     print(json.dumps(out, indent=1))
 
 
+CLASSES = {"k_scatter": "scatter", "k_hist_pre": "hist", "k_local": "local", "k_local_pipe": "local",
+           "k_local_cluster": "local", "k_children": "children"}
+
+
+def steptraffic(path, sorts):
+    """DRAM bytes (read + write) per sort of each kernel class bench.py times, from a
+    --metrics launch list of `sorts` sorts (bench.py divides by its launches per step)."""
+    rows = [r for r in csv.DictReader(l for l in open(path) if l.startswith('"'))]
+    by = collections.defaultdict(dict)
+    for r in rows:
+        d = by[int(r["ID"])]
+        d["name"] = short(r["Kernel Name"]).split("<")[0]
+        d[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * UNIT.get(r["Metric Unit"], 1)
+    fam = collections.defaultdict(float)
+    for d in by.values():
+        if d["name"] in CLASSES:
+            fam[CLASSES[d["name"]]] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    out = {k: round(v / sorts) for k, v in fam.items()}
+    out["_per"] = "step"
+    out["_source"] = (f"ncu launch list {path.split('/')[-1]} ({sorts} sorts): dram__bytes_read.sum + "
+                      "dram__bytes_write.sum summed per kernel class, per sort")
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
     cmd, arg = sys.argv[1], sys.argv[2]
     if cmd == "launches":
         launches(arg)
     elif cmd == "full":
         full(arg, int(sys.argv[sys.argv.index("--lines") + 1]) if "--lines" in sys.argv else 12)
+    elif cmd == "steptraffic":
+        steptraffic(arg, int(sys.argv[3]))
     elif cmd == "traffic":
         traffic(arg, {a.split("=")[0]: int(a.split("=")[1]) for a in sys.argv[3:] if "=" in a})
     else:
