@@ -52,6 +52,7 @@ struct Context {
   // device, and the max active clusters of each cluster kernel on this device
   std::set<const void*> smem_attr_set;
   std::map<const void*, int> max_clusters;
+  std::map<const void*, int> occupancy;  // resident CTAs per SM of a kernel at its launch shape
   Ctl* h_ctl = nullptr;  // pinned
   uint32_t epoch = 0;
   cudaEvent_t ev[2 * 64] = {};
@@ -82,6 +83,17 @@ template <class F>
 inline void smem_attr(Context* ctx, F* f, int bytes) {
   if (ctx->smem_attr_set.insert((const void*)f).second)
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// resident CTAs per SM of kernel f at (threads, dynamic smem), cached per device
+template <class F>
+inline int occupancy(Context* ctx, F* f, int threads, size_t smem) {
+  auto it = ctx->occupancy.find((const void*)f);
+  if (it != ctx->occupancy.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, threads, smem) != cudaSuccess) occ = 0;
+  ctx->occupancy[(const void*)f] = occ;
+  return occ;
 }
 
 // NVTX range for the host-side phases (the MSD level, the multi-GPU steps)

@@ -576,6 +576,24 @@ __device__ __noinline__ void split_tile(const Seg sg, uint32_t s, uint32_t base,
 // Tiles come from an atomic ticket so look-back only waits on running CTAs.
 constexpr int SCATTER_PAD = 64;  // dynamic smem beyond the TB-byte tile: the pad slot of absent records
 
+// TMA write-out of a record size that is an odd multiple of 8 bytes (8, 24, 40):
+// a run is 16-byte aligned in HBM only from an even record position, so each
+// digit's run is staged at the parity of its global position (one spare slot
+// per digit, DG + 1 more slots); its odd head / tail record leaves as a plain
+// store, the even middle as one bulk copy
+template <int R, int TB, int SB, int DB, bool TMA_OUT>
+__host__ __device__ constexpr bool scatter_parity() { return TMA_OUT && R % 16 != 0; }
+template <int R, int TB, int SB, int DB, bool TMA_OUT>
+__host__ __device__ constexpr uint32_t scatter_padslot() {
+  return scatter_parity<R, TB, SB, DB, TMA_OUT>() ? tile_recs<R, TB, SB>() + (1u << DB) + 1u : tile_recs<R, TB, SB>();
+}
+template <int R, int TB, int SB, int DB, bool TMA_OUT>
+__host__ __device__ constexpr size_t scatter_smem() {
+  return scatter_parity<R, TB, SB, DB, TMA_OUT>()
+             ? (((size_t)(scatter_padslot<R, TB, SB, DB, TMA_OUT>() + 1u) * R + 15) & ~(size_t)15)
+             : (size_t)TB + SCATTER_PAD;
+}
+
 template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false, int DB = 8, bool TMA_OUT = false>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
@@ -597,7 +615,9 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
   // TMA write-out: every digit's staged run leaves as one bulk copy (cp.async.bulk
   // shared -> global, issued by the digit's thread) that drains while the next
   // tile is loaded, ranked and scanned; needs 16-byte aligned runs (R = 16, 32)
-  constexpr bool TW = TMA_OUT && PRE && !PEER && (R == 16 || R == 32);
+  constexpr bool TW = TMA_OUT && PRE && !PEER;
+  constexpr bool TWP = TW && scatter_parity<R, TB, SB, DB, TMA_OUT>();  // runs staged at their HBM parity
+  constexpr uint32_t PADSLOT = scatter_padslot<R, TB, SB, DB, TW>();     // the stage slot of absent records
   extern __shared__ uint4 smem_raw[];
   uint8_t* stage = reinterpret_cast<uint8_t*>(smem_raw);
   __shared__ uint32_t cnt[DG + 1], start[DG], gofs[DG], ws[(DPT == 1 ? DG : SB) / 32];  // cnt[DG]: absent records
@@ -719,6 +739,13 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
         ex[0] = block_excl_scan<SB>(c[0] + c[1], ws);
         ex[1] = ex[0] + c[0];
       }
+      if constexpr (TWP) {  // stage slot of the run = ex + digit + parity fix (<= 1): same parity as its HBM slot
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {
+          const uint32_t e = ex[j] + (uint32_t)(tid * DPT + j);
+          ex[j] = e + ((e ^ pre_excl[j]) & 1u);
+        }
+      }
       if (has_dg) {
 #pragma unroll
         for (int j = 0; j < DPT; ++j) start[tid * DPT + j] = ex[j];
@@ -730,7 +757,7 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
       for (int i = 0; i < I; ++i) {
         const uint32_t idx = (uint32_t)(i * SB + tid);
         const uint32_t pos = start[digit_w<DB>(key_of<R, K>(r[i]), d)] + ((rk[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-        st_rec<R>(stage + (size_t)(idx < m ? pos : T) * R, r[i]);
+        st_rec<R>(stage + (size_t)(idx < m ? pos : PADSLOT) * R, r[i]);
       }
       if constexpr (TW) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staged -> visible to TMA
       __syncthreads();  // r[] free, sh_t/sh_s hold the next ticket
@@ -745,11 +772,22 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
           bool any = false;
 #pragma unroll
           for (int j = 0; j < DPT; ++j) {
-            if (c[j]) {
-              const uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + (size_t)ex[j] * R);
-              uint8_t* ga = dst + (size_t)pre_excl[j] * R;
+            uint32_t cc = c[j], sp = ex[j], g = pre_excl[j];
+            if constexpr (TWP) {  // odd head / tail records: plain stores (16-byte bulk alignment)
+              if (cc && (g & 1u)) {
+                st_rec<R>(dst + (size_t)g * R, ld_rec<R>(stage + (size_t)sp * R));
+                ++g; ++sp; --cc;
+              }
+              if (cc & 1u) {
+                --cc;
+                st_rec<R>(dst + (size_t)(g + cc) * R, ld_rec<R>(stage + (size_t)(sp + cc) * R));
+              }
+            }
+            if (cc) {
+              const uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + (size_t)sp * R);
+              uint8_t* ga = dst + (size_t)g * R;
               asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(ga), "r"(sa),
-                           "r"(c[j] * (uint32_t)R)
+                           "r"(cc * (uint32_t)R)
                            : "memory");
               any = true;
             }

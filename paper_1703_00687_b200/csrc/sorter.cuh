@@ -64,7 +64,11 @@ struct Sorter {
   }
   static bool pipe_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE");
-    return !(e && e[0] == '0');
+    // 1 (default): every R but 8; 2: every R; 0: plain coalesced write-out everywhere.  R = 8, 24, 40
+    // stage their runs at the parity of their HBM slot; measured (ms per sort, 2 vs 0): (24,8) 900 M
+    // 44.7 / 48.7, (24,16) 48.7 / 49.5, (40,16) 500 M 52.4 / 53.0, but (8,8) 1 G 17.4 / 16.9
+    const int mode = e ? atoi(e) : 1;
+    return mode == 2 || (mode == 1 && R != 8);
   }
 
 
@@ -407,7 +411,11 @@ struct Sorter {
   // c4 level-0 scatter 11.8 -> 10.3 ms, c2 2.39 -> 2.16 ms)
   static bool scatter_tma() {
     const char* e = getenv("RADSORT_SCATTER_TMA");
-    return (R == 16 || R == 32) && !(e && e[0] == '0');
+    // 1 (default): every R but 8; 2: every R; 0: plain coalesced write-out everywhere.  R = 8, 24, 40
+    // stage their runs at the parity of their HBM slot; measured (ms per sort, 2 vs 0): (24,8) 900 M
+    // 44.7 / 48.7, (24,16) 48.7 / 49.5, (40,16) 500 M 52.4 / 53.0, but (8,8) 1 G 17.4 / 16.9
+    const int mode = e ? atoi(e) : 1;
+    return mode == 2 || (mode == 1 && R != 8);
   }
 
   // One Large level: tile map, histogram + cross-tile prefix, plan, scatter,
@@ -450,10 +458,15 @@ struct Sorter {
     }
     const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
     tm.begin(RADSORT_K_SCATTER);
-    if (pre && scatter_tma()) {
-      auto* kfn = k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true>;
-      smem_attr(ctx, kfn, TB_ + SCATTER_PAD);
-      kfn<<<gs, SB_, TB_ + SCATTER_PAD, st>>>(L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs,
+    auto* kfn_tw = k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true>;
+    constexpr size_t sm_tw = scatter_smem<R, TB_, SB_, DB, true>();
+    // (the parity-staged stage of R = 40 on a wide level would cost a CTA per SM: plain write-out there)
+    const bool tw = pre && scatter_tma() && (((uintptr_t)recs | (uintptr_t)tmp) & 15u) == 0;  // bulk copies: 16-byte aligned
+    if (tw) smem_attr(ctx, kfn_tw, sm_tw);
+    if (tw && occupancy(ctx, kfn_tw, SB_, sm_tw) >= MINB_) {
+      auto* kfn = kfn_tw;
+      constexpr size_t sm = sm_tw;
+      kfn<<<gs, SB_, sm, st>>>(L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs,
                                               tmp, v.tile_pre, ch_first, carry_in, hist_grid, v.splitc, v.probes,
                                               v.tile_seg, nullptr);
     } else if (pre)

@@ -89,6 +89,17 @@ def test_other_tile_configs(cfg, monkeypatch):
         check(dg.generate(400_003, R, K, "zipf", seed=13), K)
 
 
+@pytest.mark.parametrize("tma", ["0", "1", "2"])
+def test_scatter_write_out_paths(tma, monkeypatch):
+    # the radix pass's write-out: coalesced plain stores (0) or one bulk copy per digit run (1: R = 16, 32;
+    # 2: every R); R = 8, 24, 40 stage each run at the parity of its HBM slot and store an odd head / tail
+    # record by hand -- odd and even run starts / lengths everywhere in these inputs
+    monkeypatch.setenv("RADSORT_SCATTER_TMA", tma)
+    for R, K in LAYOUTS:
+        for n, dist in ((400_003, "uniform"), (300_001, "zipf"), (250_001, "few"), (700_001, "bytes")):
+            check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=n + R), K)
+
+
 @pytest.mark.parametrize("R,K", LAYOUTS)
 @pytest.mark.parametrize("dist", ["uniform", "uniform40", "zipf", "equal", "sorted", "reverse", "few", "consttop",
                                   "bytes"])
