@@ -64,13 +64,8 @@ struct Sorter {
   }
   static bool pipe_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE");
-    // 1 (default): every R but 8; 2: every R; 0: plain coalesced write-out everywhere.  R = 8, 24, 40
-    // stage their runs at the parity of their HBM slot; measured (ms per sort, 2 vs 0): (24,8) 900 M
-    // 44.7 / 48.7, (24,16) 48.7 / 49.5, (40,16) 500 M 52.4 / 53.0, but (8,8) 1 G 17.4 / 16.9
-    const int mode = e ? atoi(e) : 1;
-    return mode == 2 || (mode == 1 && R != 8);
+    return !(e && e[0] == '0');
   }
-
 
   // ---- the largest local bins: k_local_big (1024 threads, one bin per SM) with
   // RADSORT_LOCAL_BIG=1; k_local at 512 threads otherwise
@@ -413,7 +408,7 @@ struct Sorter {
     const char* e = getenv("RADSORT_SCATTER_TMA");
     // 1 (default): every R but 8; 2: every R; 0: plain coalesced write-out everywhere.  R = 8, 24, 40
     // stage their runs at the parity of their HBM slot; measured (ms per sort, 2 vs 0): (24,8) 900 M
-    // 44.7 / 48.7, (24,16) 48.7 / 49.5, (40,16) 500 M 52.4 / 53.0, but (8,8) 1 G 17.4 / 16.9
+    // 44.7 / 48.7, (24,16) 48.7 / 49.5, (40,16) 500 M 52.4 / 53.0, but c5 (8,8) 17.0 / 16.5
     const int mode = e ? atoi(e) : 1;
     return mode == 2 || (mode == 1 && R != 8);
   }
