@@ -19,7 +19,10 @@
 
 namespace radsort {
 
-template <int R, int K, int IL, int LB>
+// EF (early finish): bin i's fix-up and bulk store are issued right after it is
+// staged, while bin i+1's loads are in flight, instead of beside bin i+1's
+// counting atomics (which then wait on those loads)
+template <int R, int K, int IL, int LB, bool EF = true>
 __global__ void __launch_bounds__(LB, 1)
     k_local_pipe(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes,
                  uint32_t cnt_bytes, uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
@@ -188,9 +191,8 @@ __global__ void __launch_bounds__(LB, 1)
         RS_PROF(2);
         if (pending && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         pending = false;
-        RS_PROF(3);
         __syncthreads();  // starts in place; the stage is free
-        RS_PROF(4);
+        RS_PROF(3);
         break;
       }
       // every record in one bucket: skip the constant digits
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(LB, 1)
         }
       }
     }
+    RS_PROF(5);
     // registers are free: the next bin's loads overlap this bin's finish
     uint32_t nb = bi + gridDim.x;
     while (nb < nlist && skip(nb)) nb += gridDim.x;
@@ -261,9 +264,8 @@ __global__ void __launch_bounds__(LB, 1)
     }
     prefetch_l2(nb + gridDim.x);
     done += n;
-    RS_PROF(5);
+    RS_PROF(4);
     __syncthreads();  // staged
-    RS_PROF(6);
     if (!all_equal) {
       p_live = true;
       p_stg = stg;
@@ -281,6 +283,16 @@ __global__ void __launch_bounds__(LB, 1)
     }
     par = q;
     zero_cnt(2u << W);
+    RS_PROF(6);
+    if constexpr (EF) {
+      if (p_live) {
+        fixup();
+        __syncthreads();  // fix-ups done; the big-bucket list complete
+        RS_PROF(1);
+        finish();
+        p_live = false;
+      }
+    }
     RS_PROF(7);
     if (nb >= nlist) break;
     bi = nb;

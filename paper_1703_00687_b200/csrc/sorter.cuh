@@ -33,10 +33,11 @@ struct Sorter {
       // one bin per SM: the bin-pipelined variant (k_local_pipe).  Measured and dropped: the
       // same at 1024 threads (c5 local 6.74 -> 6.52 ms but c3 5.06 -> 5.23 ms, 18 B of spills)
       if (pipe_on()) {
-        smem_attr(ctx, k_local_pipe<R, K, IL, LB>, (int)LOCAL_SMEM_MAX);
+        auto* kfn = early_on() ? k_local_pipe<R, K, IL, LB, true> : k_local_pipe<R, K, IL, LB, false>;
+        smem_attr(ctx, kfn, (int)LOCAL_SMEM_MAX);
         const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms);
-        k_local_pipe<R, K, IL, LB><<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes,
-                                                         cap, next, nxt, ctl, recs, tmp, lmin, lmax, wdelta());
+        kfn<<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt, ctl, recs,
+                                 tmp, lmin, lmax, wdelta());
         return;
       }
     }
@@ -61,6 +62,14 @@ struct Sorter {
   static int wdelta() {
     const char* e = getenv("RADSORT_LOCAL_WDELTA");
     return e ? atoi(e) : 0;
+  }
+  // k_local_pipe<EF>: a bin's fix-up and bulk store issued before the next bin's count, while its
+  // loads are in flight (default; measured c4 local 16.97 -> 15.26 ms, c5 / c2 unchanged);
+  // RADSORT_LOCAL_EARLY=0: beside the next bin's counting atomics.  Measured and dropped: a
+  // branch-free count (absent records counted in pad words): c4 15.26 -> 15.57, c5 6.70 -> 9.02 (spills)
+  static bool early_on() {
+    const char* e = getenv("RADSORT_LOCAL_EARLY");
+    return !(e && e[0] == '0');
   }
   static bool pipe_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE");
@@ -404,8 +413,15 @@ struct Sorter {
 
   // the scatter's digit runs leave by TMA bulk copies (R = 16, 32; RADSORT_SCATTER_TMA=0: thread stores;
   // c4 level-0 scatter 11.8 -> 10.3 ms, c2 2.39 -> 2.16 ms)
-  static bool scatter_tma() {
+  // shortest digit run the TMA write-out sends as a bulk copy (shorter runs: stored by the digit's
+  // thread); RADSORT_SCATTER_TWMIN / RADSORT_SCATTER_TWMIN_WIDE for 8-bit / 10-bit levels (1, 2, 4)
+  static int scatter_twmin(int db) {
+    const char* e = getenv(db == 8 ? "RADSORT_SCATTER_TWMIN" : "RADSORT_SCATTER_TWMIN_WIDE");
+    return e ? atoi(e) : 1;
+  }
+  static bool scatter_tma(int db) {
     const char* e = getenv("RADSORT_SCATTER_TMA");
+    if (e && e[0] == '3') return db == 8;  // (experiment: 8-bit levels only)
     // 1 (default): every R but 8; 2: every R; 0: plain coalesced write-out everywhere.  R = 8, 24, 40
     // stage their runs at the parity of their HBM slot; measured (ms per sort, 2 vs 0): (24,8) 900 M
     // 44.7 / 48.7, (24,16) 48.7 / 49.5, (40,16) 500 M 52.4 / 53.0, but c5 (8,8) 17.0 / 16.5
@@ -453,17 +469,17 @@ struct Sorter {
     }
     const unsigned gs = (unsigned)std::min(tiles_ub, (size_t)ctx->sms * occ_s);
     tm.begin(RADSORT_K_SCATTER);
-    auto* kfn_tw = k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true>;
-    constexpr size_t sm_tw = scatter_smem<R, TB_, SB_, DB, true>();
     // (the parity-staged stage of R = 40 on a wide level would cost a CTA per SM: plain write-out there)
-    const bool tw = pre && scatter_tma() && (((uintptr_t)recs | (uintptr_t)tmp) & 15u) == 0;  // bulk copies: 16-byte aligned
+    constexpr size_t sm_tw = scatter_smem<R, TB_, SB_, DB, true>();
+    const int twm = scatter_twmin(DB);
+    auto* kfn_tw = twm >= 4 ? k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true, 4>
+                            : (twm == 2 ? k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true, 2>
+                                        : k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true, 1>);
+    const bool tw = pre && scatter_tma(DB) && (((uintptr_t)recs | (uintptr_t)tmp) & 15u) == 0;  // bulk copies: 16-byte aligned
     if (tw) smem_attr(ctx, kfn_tw, sm_tw);
     if (tw && occupancy(ctx, kfn_tw, SB_, sm_tw) >= MINB_) {
-      auto* kfn = kfn_tw;
-      constexpr size_t sm = sm_tw;
-      kfn<<<gs, SB_, sm, st>>>(L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs,
-                                              tmp, v.tile_pre, ch_first, carry_in, hist_grid, v.splitc, v.probes,
-                                              v.tile_seg, nullptr);
+      kfn_tw<<<gs, SB_, sm_tw, st>>>(L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp,
+                                     v.tile_pre, ch_first, carry_in, hist_grid, v.splitc, v.probes, v.tile_seg, nullptr);
     } else if (pre)
       k_scatter<R, K, TB_, SB_, MINB_, true, false, DB><<<gs, SB_, TB_ + SCATTER_PAD, st>>>(
           L[cur], v.tile_start, n_large, v.segbase, v.status, ctx->epoch, v.ctl, recs, tmp, v.tile_pre, ch_first,
