@@ -594,8 +594,7 @@ __host__ __device__ constexpr size_t scatter_smem() {
              : (size_t)TB + SCATTER_PAD;
 }
 
-template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false, int DB = 8, bool TMA_OUT = false,
-          int TWMIN = 1>
+template <int R, int K, int TB, int SB, int MINB, bool PRE, bool PEER = false, int DB = 8, bool TMA_OUT = false>
 __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ segs, const uint32_t* __restrict__ tile_start,
                                                        uint32_t nseg, const uint32_t* __restrict__ segbase,
                                                        unsigned long long* __restrict__ status, uint32_t epoch, Ctl* ctl,
@@ -774,11 +773,6 @@ __global__ void __launch_bounds__(SB, MINB) k_scatter(const Seg* __restrict__ se
 #pragma unroll
           for (int j = 0; j < DPT; ++j) {
             uint32_t cc = c[j], sp = ex[j], g = pre_excl[j];
-            if (TWMIN > 1 && cc < (uint32_t)TWMIN) {  // a short run: the digit's thread stores it (a bulk
-              for (uint32_t k = 0; k < cc; ++k)        // copy costs ~12 warp instructions to issue)
-                st_rec<R>(dst + (size_t)(g + k) * R, ld_rec<R>(stage + (size_t)(sp + k) * R));
-              cc = 0;
-            }
             if constexpr (TWP) {  // odd head / tail records: plain stores (16-byte bulk alignment)
               if (cc && (g & 1u)) {
                 st_rec<R>(dst + (size_t)g * R, ld_rec<R>(stage + (size_t)sp * R));

@@ -413,12 +413,10 @@ struct Sorter {
 
   // the scatter's digit runs leave by TMA bulk copies (R = 16, 32; RADSORT_SCATTER_TMA=0: thread stores;
   // c4 level-0 scatter 11.8 -> 10.3 ms, c2 2.39 -> 2.16 ms)
-  // shortest digit run the TMA write-out sends as a bulk copy (shorter runs: stored by the digit's
-  // thread); RADSORT_SCATTER_TWMIN / RADSORT_SCATTER_TWMIN_WIDE for 8-bit / 10-bit levels (1, 2, 4)
-  static int scatter_twmin(int db) {
-    const char* e = getenv(db == 8 ? "RADSORT_SCATTER_TWMIN" : "RADSORT_SCATTER_TWMIN_WIDE");
-    return e ? atoi(e) : 1;
-  }
+  // Measured and dropped (c4, ms per pass): runs shorter than 2 / 4 records stored by the digit's
+  // thread instead of a bulk copy (whose issue costs ~12 warp instructions: the operands go to
+  // uniform registers lane by lane): wide level 13.57 -> 14.65 / 18.29, 8-bit level 10.2 -> 10.2 / 12.2;
+  // the wide level's plain write-out (RADSORT_SCATTER_TMA=3): 14.55
   static bool scatter_tma(int db) {
     const char* e = getenv("RADSORT_SCATTER_TMA");
     if (e && e[0] == '3') return db == 8;  // (experiment: 8-bit levels only)
@@ -471,10 +469,7 @@ struct Sorter {
     tm.begin(RADSORT_K_SCATTER);
     // (the parity-staged stage of R = 40 on a wide level would cost a CTA per SM: plain write-out there)
     constexpr size_t sm_tw = scatter_smem<R, TB_, SB_, DB, true>();
-    const int twm = scatter_twmin(DB);
-    auto* kfn_tw = twm >= 4 ? k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true, 4>
-                            : (twm == 2 ? k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true, 2>
-                                        : k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true, 1>);
+    auto* kfn_tw = k_scatter<R, K, TB_, SB_, MINB_, true, false, DB, true>;
     const bool tw = pre && scatter_tma(DB) && (((uintptr_t)recs | (uintptr_t)tmp) & 15u) == 0;  // bulk copies: 16-byte aligned
     if (tw) smem_attr(ctx, kfn_tw, sm_tw);
     if (tw && occupancy(ctx, kfn_tw, SB_, sm_tw) >= MINB_) {
