@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(LB, 1)
       first = false;
       RS_PROF(1);
       if (!s_const) {
-        local_scan<LB>(cnt, W, wsum);
+        local_scan<LB, R == 8 ? 2 : 1>(cnt, W, wsum);  // (c5 local 6.70 -> 6.51 ms; R >= 16 lose)
         RS_PROF(2);
         if (pending && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         pending = false;

@@ -1102,8 +1102,11 @@ __host__ __device__ __forceinline__ uint32_t local_width(uint32_t n, uint32_t wm
 // contiguous chunk per warp, 16-byte accesses, the two halves of a word summed
 // as one 32-bit add (no half overflows: every count and sum is <= n <= 2^14).
 // Contains one block barrier; the caller synchronises after it.
-template <int LB>
+// U = 2: two 32-uint4 blocks per step with interleaved shuffle scans (more ILP,
+// more live registers: measured a win for k_local_pipe on R = 8 only)
+template <int LB, int U = 1>
 __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* wsum) {
+  static_assert(U == 1 || U == 2, "one or two blocks per step");
   constexpr int NW = LB / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t pw = (1u << (W - 1)) / NW;  // words per warp, a multiple of 4
@@ -1120,26 +1123,39 @@ __device__ __forceinline__ void local_scan(uint32_t* cnt, uint32_t W, uint32_t* 
   // carry-in of this warp's chunk: exclusive prefix of the warp totals (lane w holds warp w's)
   uint32_t carry = (lane < NW && lane < warp) ? wsum[lane] : 0u;
   carry = __reduce_add_sync(0xffffffffu, carry);
-  for (uint32_t j0 = 0; j0 < n4; j0 += 32) {
-    const uint32_t j = j0 + lane;
-    const uint4 v = j < n4 ? c4[j] : make_uint4(0, 0, 0, 0);
-    const uint32_t p = v.x + v.y + v.z + v.w;
-    const uint32_t t = (p & 0xffffu) + (p >> 16);
-    uint32_t inc = t;
+  for (uint32_t j0 = 0; j0 < n4; j0 += 32 * U) {
+    uint4 v[U];
+    uint32_t t[U], inc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + 32u * u + lane;
+      v[u] = j < n4 ? c4[j] : make_uint4(0, 0, 0, 0);
+      const uint32_t p = v[u].x + v[u].y + v[u].z + v[u].w;
+      t[u] = (p & 0xffffu) + (p >> 16);
+      inc[u] = t[u];
+    }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc[u], o);
+        if (lane >= o) inc[u] += y;
+      }
     }
-    // word start (both halves) = s | s << 16, then + (lo << 16) for the high half
-    uint32_t s = carry + inc - t;
-    uint4 o4;
-    o4.x = s * 0x10001u + (v.x << 16); s += (v.x & 0xffffu) + (v.x >> 16);
-    o4.y = s * 0x10001u + (v.y << 16); s += (v.y & 0xffffu) + (v.y >> 16);
-    o4.z = s * 0x10001u + (v.z << 16); s += (v.z & 0xffffu) + (v.z >> 16);
-    o4.w = s * 0x10001u + (v.w << 16);
-    if (j < n4) c4[j] = o4;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
+    const uint32_t tot0 = __shfl_sync(0xffffffffu, inc[0], 31);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + 32u * u + lane;
+      // word start (both halves) = s | s << 16, then + (lo << 16) for the high half
+      uint32_t s = carry + (u ? tot0 : 0u) + inc[u] - t[u];
+      uint4 o4;
+      o4.x = s * 0x10001u + (v[u].x << 16); s += (v[u].x & 0xffffu) + (v[u].x >> 16);
+      o4.y = s * 0x10001u + (v[u].y << 16); s += (v[u].y & 0xffffu) + (v[u].y >> 16);
+      o4.z = s * 0x10001u + (v[u].z << 16); s += (v[u].z & 0xffffu) + (v[u].z >> 16);
+      o4.w = s * 0x10001u + (v[u].w << 16);
+      if (j < n4) c4[j] = o4;
+    }
+    carry += tot0 + (U > 1 ? __shfl_sync(0xffffffffu, inc[U - 1], 31) : 0u);
   }
 }
 
