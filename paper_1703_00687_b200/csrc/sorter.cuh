@@ -115,6 +115,10 @@ struct Sorter {
     const char* m = getenv("RADSORT_LOCAL2_MIN");
     return m ? (uint32_t)atoi(m) : 4096u;
   }
+  static uint32_t l2_gcap() {  // smallest group k_local2 hands back as a Large bin (+1)
+    if constexpr (L2_BUILT) return (uint32_t)L2Cfg<R>::GCAP;
+    return C;
+  }
   static uint32_t local_max() {  // the largest bin the Local list takes
     if constexpr (L2_BUILT) {
       if (local2_min() != 0xffffffffu) return std::max(C, local2_max<R>());
@@ -357,7 +361,8 @@ struct Sorter {
   // extra: initial segments of a presegmented input (multi-GPU receive side), any size
   static radsort_status prepare(Context* ctx, uint32_t n, uint32_t T, Views& v, bool lookback = false,
                                 uint32_t extra = 0) {
-    const size_t capL = (size_t)n / C + 4 + extra;
+    // Large bins hold > C records, except the skewed groups k_local2 hands back (> its GCAP)
+    const size_t capL = (size_t)n / (local2_min() != 0xffffffffu ? l2_gcap() : C) + 4 + extra;
     // Local bins: children of > TINY_MAX records, or mixed buckets of > ES_MAX records queued by
     // the cluster / pipelined local sorts
     const size_t capLoc = (size_t)n / (es_max<R>() + 1) + 4 + extra;
