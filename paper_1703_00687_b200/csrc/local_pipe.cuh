@@ -23,7 +23,7 @@ namespace radsort {
 // staged, while bin i+1's loads are in flight, instead of beside bin i+1's
 // counting atomics (which then wait on those loads)
 template <int R, int K, int IL, int LB, bool EF = true>
-__global__ void __launch_bounds__(LB, 1)
+__global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     k_local_pipe(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes,
                  uint32_t cnt_bytes, uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
                  uint32_t lmin, uint32_t lmax, int wdelta) {

@@ -29,13 +29,16 @@ struct Sorter {
     while (wmax > LOCAL_WMIN && stage_bytes + cnt_of(wmax) + big_bytes > LOCAL_SMEM_MAX) --wmax;
     const size_t cnt_bytes = cnt_of(wmax);
     const size_t smem = stage_bytes + cnt_bytes + big_bytes;
-    if constexpr (LB == 512) {
-      // one bin per SM: the bin-pipelined variant (k_local_pipe).  Measured and dropped: the
-      // same at 1024 threads (c5 local 6.74 -> 6.52 ms but c3 5.06 -> 5.23 ms, 18 B of spills)
-      if (pipe_on()) {
+    if constexpr (LB == 512 || LB == 256) {
+      // one bin per SM (512 threads) or two (256): the bin-pipelined variant (k_local_pipe).
+      // Measured and dropped: the same at 1024 threads (c5 local 6.74 -> 6.52 ms but c3 5.06 ->
+      // 5.23 ms, 18 B of spills)
+      if (pipe_on() && (LB == 512 || pipe256_on())) {
         auto* kfn = early_on() ? k_local_pipe<R, K, IL, LB, true> : k_local_pipe<R, K, IL, LB, false>;
         smem_attr(ctx, kfn, (int)LOCAL_SMEM_MAX);
-        const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms);
+        int occ = 1;
+        if (LB < 512) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, LB, smem);
+        const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
         kfn<<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt, ctl, recs,
                                  tmp, lmin, lmax, wdelta());
         return;
@@ -70,6 +73,13 @@ struct Sorter {
   static bool early_on() {
     const char* e = getenv("RADSORT_LOCAL_EARLY");
     return !(e && e[0] == '0');
+  }
+  // the 256-thread (two CTAs per SM) local sorts pipelined too: default for R >= 16 (measured
+  // c2 local 1.81 -> 1.56 ms, kmc unchanged; c3 (R = 8, Zipf) 5.19 -> 5.51 ms: off for R = 8);
+  // RADSORT_LOCAL_PIPE256=1 / 0 forces it on / off
+  static bool pipe256_on() {
+    const char* e = getenv("RADSORT_LOCAL_PIPE256");
+    return e ? e[0] == '1' : R >= 16;
   }
   static bool pipe_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE");

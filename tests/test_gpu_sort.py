@@ -414,13 +414,14 @@ def test_rare_wide_outliers(R, K):
     check(a, K)
 
 
-@pytest.mark.parametrize("var", ["RADSORT_LOCAL_BIG=1", "RADSORT_LOCAL2=1", "RADSORT_LOCAL_EARLY=0", "RADSORT_LOCAL_PIPE=0"])
+@pytest.mark.parametrize("var", ["RADSORT_LOCAL_BIG=1", "RADSORT_LOCAL2=1", "RADSORT_LOCAL_EARLY=0", "RADSORT_LOCAL_PIPE=0",
+                                 "RADSORT_LOCAL_PIPE256=1", "RADSORT_LOCAL_PIPE256=0"])
 @pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (16, 16), (32, 16), (24, 8), (40, 16)])
 def test_opt_in_local_sorters(var, R, K, monkeypatch):
     # the opt-in local sorters (k_local_big: 1024-thread CTAs, ranks by a second
     # atomic pass; k_local2: two-phase partition through the scratch range; the
     # pipelined sort with a bin's fix-up beside the next bin's count; round 1's
-    # unpipelined k_local) on bins of every size class, skewed and duplicate-heavy keys included
+    # unpipelined k_local; the 256-thread class pipelined or not) on bins of every size class, skewed and duplicate-heavy keys included
     name, val = var.split("=")
     monkeypatch.setenv(name, val)
     for dist, n in (("uniform", 2_000_003), ("zipf", 1_500_001), ("few", 300_007), ("bytes", 700_001),
