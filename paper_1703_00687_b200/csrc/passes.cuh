@@ -1493,25 +1493,6 @@ __global__ void __launch_bounds__(LB, LB <= 64 ? 8 : (LB <= 256 ? 2 : 1))
 
 // L2-coherent loads (.cg: the SM's L1 may hold lines of the bin read before
 // the cluster's other CTAs wrote them)
-template <int R> __device__ __forceinline__ Rec<R> ldcg_rec(const uint8_t* p);
-template <> __device__ __forceinline__ Rec<32> ldcg_rec<32>(const uint8_t* p) {
-  Rec<32> r;
-  asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r.a.x), "=r"(r.a.y), "=r"(r.a.z), "=r"(r.a.w), "=r"(r.b.x), "=r"(r.b.y), "=r"(r.b.z), "=r"(r.b.w)
-               : "l"(p)
-               : "memory");
-  return r;
-}
-template <> __device__ __forceinline__ Rec<16> ldcg_rec<16>(const uint8_t* p) { return {__ldcg(reinterpret_cast<const uint4*>(p))}; }
-template <> __device__ __forceinline__ Rec<8> ldcg_rec<8>(const uint8_t* p) { return {__ldcg(reinterpret_cast<const uint2*>(p))}; }
-template <> __device__ __forceinline__ Rec<24> ldcg_rec<24>(const uint8_t* p) {
-  const uint2* q = reinterpret_cast<const uint2*>(p);
-  return {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2)};
-}
-template <> __device__ __forceinline__ Rec<40> ldcg_rec<40>(const uint8_t* p) {
-  const uint2* q = reinterpret_cast<const uint2*>(p);
-  return {__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4)};
-}
 
 template <int R, int K>
 __device__ __forceinline__ void cswap_rec(Rec<R>& a, Rec<R>& b) {
