@@ -26,7 +26,7 @@ template <int R, int K, int IL, int LB, bool EF = true>
 __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
     k_local_pipe(const Seg* __restrict__ list, uint32_t nlist, uint32_t wmax, uint32_t stage_bytes,
                  uint32_t cnt_bytes, uint32_t cap, Seg* local_next, int nxt, Ctl* ctl, uint8_t* recs, uint8_t* tmp,
-                 uint32_t lmin, uint32_t lmax, int wdelta) {
+                 uint32_t lmin, uint32_t lmax, int wdelta, uint32_t pfd) {
   extern __shared__ uint4 smem_raw[];
   constexpr int KW = K / 8;
   constexpr int NW = LB / 32;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
   };
   Seg sg = list[bi];
   load(sg);
-  prefetch_l2(bi + gridDim.x);
+  for (uint32_t k = 1; k <= pfd; ++k) prefetch_l2(bi + k * gridDim.x);
   zero_cnt(cnt_bytes);
   if (tid < 2) { sna[tid] = 0; so[tid] = 0; s_ncol[tid] = 0; s_nbig[tid] = 0; }
   if (tid == 0) s_const = 0;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1)
       nsg = list[nb];
       load(nsg);
     }
-    prefetch_l2(nb + gridDim.x);
+    if (pfd) prefetch_l2(nb + pfd * gridDim.x);  // the bin pfd ahead of the one being loaded streams into L2
     done += n;
     RS_PROF(4);
     __syncthreads();  // staged

@@ -40,7 +40,7 @@ struct Sorter {
         if (LB < 512) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, LB, smem);
         const unsigned g = (unsigned)std::min<size_t>(nloc, (size_t)sms * std::max(occ, 1));
         kfn<<<g, LB, smem, st>>>(list, nloc, wmax, (uint32_t)stage_bytes, (uint32_t)cnt_bytes, cap, next, nxt, ctl, recs,
-                                 tmp, lmin, lmax, wdelta());
+                                 tmp, lmin, lmax, wdelta(), pf_dist());
         return;
       }
     }
@@ -80,6 +80,10 @@ struct Sorter {
   static bool pipe256_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE256");
     return e ? e[0] == '1' : R >= 16;
+  }
+  static uint32_t pf_dist() {  // k_local_pipe: how many bins ahead of the loaded one go to L2 (RADSORT_LOCAL_PFD)
+    const char* e = getenv("RADSORT_LOCAL_PFD");
+    return e ? (uint32_t)std::max(0, atoi(e)) : 1u;
   }
   static bool pipe_on() {
     const char* e = getenv("RADSORT_LOCAL_PIPE");
