@@ -5,8 +5,9 @@
 #   launches  ncu launch lists with DRAM bytes (c4, c5, c2, c3) -> traffic per kernel class
 #   ncu    ncu --set full of the top kernels of c4 and c5
 set -u
-O=gpurun_out/r02c_final; mkdir -p $O
+O=${OUT-gpurun_out/r02c_final}; mkdir -p $O
 STAGES=${STAGES-"tests bench launches ncu"}
+NCU_SPECS=${NCU_SPECS-"c4 k_local_pipe 0 local|c4 k_scatter 0 scatter8|c4 k_scatter 1 scatter10|c4 k_hist_pre 1 hist10|c5 k_local_pipe 0 local|c5 k_scatter 0 scatter8"}
 for st in $STAGES; do
   case $st in
   tests) timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log | cut -c1-300 ;;
@@ -25,7 +26,8 @@ for st in $STAGES; do
         --log-file $O/${c}_launches.csv python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch_$c.log 2>&1; echo "launches $c rc=$?"
     done ;;
   ncu)
-    for spec in "c4 k_local_pipe 0 local" "c4 k_scatter 0 scatter8" "c4 k_scatter 1 scatter10" "c4 k_hist_pre 1 hist10" "c5 k_local_pipe 0 local" "c5 k_scatter 0 scatter8"; do
+    IFS='|' read -ra SPECS <<< "$NCU_SPECS"
+    for spec in "${SPECS[@]}"; do
       set -- $spec
       timeout 900 ncu --set full --import-source on --clock-control none -k regex:"^$2" --launch-skip $3 -c 1 -o $O/${1}_$4 \
         python bench.py --config $1 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_${1}_$4.log 2>&1; echo "ncu $1 $4 rc=$?"
