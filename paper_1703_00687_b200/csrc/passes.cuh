@@ -79,12 +79,14 @@ __global__ void k_sample(Seg* large0, Ctl* ctl, const uint8_t* __restrict__ recs
   }
   for (int w = 0; w < KW; ++w) { atomicAnd(&sa[w], a[w]); atomicOr(&so[w], o[w]); }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // k_init's Large case, folded in (one launch fewer per sort)
     uint64_t A[2] = {sa[0], sa[1]}, O[2] = {so[0], so[1]};
     uint32_t d = first_nonconst_digit<K>(A, O, 0);
     if (d >= (uint32_t)K) d = 0;
-    large0[0].depth = (uint8_t)d;
-    ctl->d0 = d;
+    Ctl c = {};
+    c.d0 = d;
+    *ctl = c;
+    large0[0] = Seg{0u, n, (uint8_t)d, SRC_REC, MODE_NONE, 0, 0};
   }
 }
 

@@ -630,14 +630,15 @@ struct Sorter {
       level_recs = 0;
       for (const Seg& g : lg) level_recs += g.len;
     } else {
-      k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
       n_large = n > C ? 1u : 0u;
-    }
-    if (n_large && !init) {
-      tm.begin(RADSORT_K_SAMPLE);
-      k_sample<R, K><<<1, 256, 0, st>>>(L[0], ctl, recs, n);
-      tm.end();
-      stats.kernel_launches[RADSORT_K_SAMPLE]++;
+      if (n_large) {  // k_sample also writes the control block and the level-0 segment (k_init's Large case)
+        tm.begin(RADSORT_K_SAMPLE);
+        k_sample<R, K><<<1, 256, 0, st>>>(L[0], ctl, recs, n);
+        tm.end();
+        stats.kernel_launches[RADSORT_K_SAMPLE]++;
+      } else {
+        k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
+      }
     }
     int cur = 0;
     const int max_levels = 2 * K + 4;
@@ -736,9 +737,9 @@ struct Sorter {
       level_recs = c.rec_large_next;
       cur = nxt;
     }
-    // final statistics (one more small read; the sort's last kernels are ordered before it)
-    RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-    RS_CUDA(cudaStreamSynchronize(st));
+    // final statistics: the loop leaves only after a control-block read with no
+    // kernel launched since (nloc == 0 at the last level), so h_ctl is current
+    // (saves a D2H + host sync per sort: c1 is sync-bound)
     const Ctl c = *ctx->h_ctl;
 #ifdef RADSORT_PHASE_PROF
     if (log) {
