@@ -131,6 +131,26 @@ radsort_status radsort_sort(void* dev_records, void* dev_tmp, uint64_t n, uint32
 radsort_status radsort_sort_host(void* host_records, uint64_t n, uint32_t rec_size,
                                  uint32_t key_size, void* stream);
 
+/* Streaming end-to-end sort of `nbatch` independent batches on HOST memory
+ * (a sequence of sorting problems as stated at PAPER.md:35 §1, each sorted as
+ * by radsort_sort): batch k is host_in[k] (n*rec_size bytes, pinned for
+ * overlap), its sorted records land in host_out[k] (may equal host_in[k];
+ * batches may share one host_out buffer, the copies-out run in batch order).
+ * The host<->device copies are pipelined: the copy-in of batch k+1 and the
+ * copy-out of batch k-1 run on two internal streams while batch k is sorted
+ * on `stream`, so the sustained rate is bounded by the slower copy direction
+ * rather than by copy-in + sort + copy-out.  dev_bufs: nbuf >= 2 device record
+ * buffers of n*rec_size bytes (batch k is staged in dev_bufs[k % nbuf]; 3
+ * overlap the sort too), dev_tmp: one scratch buffer of n*rec_size bytes; all
+ * 16-byte aligned and non-overlapping, caller-owned, contents undefined on
+ * return.  Synchronous: returns after the last batch is in host memory.
+ * Errors as radsort_sort (plus RADSORT_ERR_INVALID_ARG for nbuf < 2 or a NULL
+ * pointer); on error, batches already copied out are complete, later ones are
+ * undefined. */
+radsort_status radsort_sort_host_stream(void* const* host_in, void* const* host_out, uint32_t nbatch,
+                                        uint64_t n, uint32_t rec_size, uint32_t key_size,
+                                        void* const* dev_bufs, uint32_t nbuf, void* dev_tmp, void* stream);
+
 /* Multi-GPU collective sort (one process per GPU; every rank of nccl_comm
  * calls it with the same rec_size/key_size).  The paper's phase 1 -- "parallel
  * processing of the whole array according to the first digit" (PAPER.md:119

@@ -216,6 +216,96 @@ radsort_status radsort_sort_host(void* host_records, uint64_t n, uint32_t rec_si
   return RADSORT_OK;
 }
 
+radsort_status radsort_sort_host_stream(void* const* host_in, void* const* host_out, uint32_t nbatch, uint64_t n,
+                                        uint32_t rec_size, uint32_t key_size, void* const* dev_bufs, uint32_t nbuf,
+                                        void* dev_tmp, void* stream) {
+  g_detail.clear();
+  radsort_status rs = check_layout(rec_size, key_size);
+  if (rs) return rs;
+  if (nbatch == 0) return RADSORT_OK;
+  if (!host_in || !host_out || !dev_bufs || !dev_tmp || nbuf < 2) {
+    set_detail("NULL pointer array or nbuf < 2");
+    return RADSORT_ERR_INVALID_ARG;
+  }
+  for (uint32_t k = 0; k < nbatch; ++k)
+    if (!host_in[k] || !host_out[k]) {
+      set_detail("NULL host buffer of batch %u", k);
+      return RADSORT_ERR_INVALID_ARG;
+    }
+  for (uint32_t b = 0; b < nbuf; ++b)
+    if (!dev_bufs[b]) {
+      set_detail("NULL device buffer %u", b);
+      return RADSORT_ERR_INVALID_ARG;
+    }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return RADSORT_ERR_CUDA; }
+  if (!get_ctx(dev)) return RADSORT_ERR_NOT_INITIALIZED;
+  const size_t bytes = (size_t)n * rec_size;
+  if (n <= 1) {
+    for (uint32_t k = 0; k < nbatch; ++k)
+      if (host_out[k] != host_in[k]) memcpy(host_out[k], host_in[k], bytes);
+    return RADSORT_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream, cin = nullptr, cout = nullptr;
+  std::vector<cudaEvent_t> ev_in(nbatch, nullptr), ev_sorted(nbatch, nullptr), ev_out(nbatch, nullptr);
+  auto cleanup = [&]() {
+    for (auto* v : {&ev_in, &ev_sorted, &ev_out})
+      for (cudaEvent_t e : *v)
+        if (e) cudaEventDestroy(e);
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
+  };
+  auto fail = [&](cudaError_t e, const char* what) {
+    set_detail("%s: %s", what, cudaGetErrorString(e));
+    cudaGetLastError();
+    if (cin) cudaStreamSynchronize(cin);
+    if (cout) cudaStreamSynchronize(cout);
+    if (st) cudaStreamSynchronize(st);
+    cleanup();
+    return RADSORT_ERR_CUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking)) ||
+      (e = cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking)))
+    return fail(e, "stream create");
+  for (uint32_t k = 0; k < nbatch; ++k)
+    if ((e = cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming)) ||
+        (e = cudaEventCreateWithFlags(&ev_sorted[k], cudaEventDisableTiming)) ||
+        (e = cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming)))
+      return fail(e, "event create");
+  // copy-in of batch k into dev_bufs[k % nbuf], once the copy-out of batch k - nbuf has read it
+  auto copy_in = [&](uint32_t k) -> cudaError_t {
+    cudaError_t r;
+    if (k >= nbuf && (r = cudaStreamWaitEvent(cin, ev_out[k - nbuf], 0))) return r;
+    if ((r = cudaMemcpyAsync(dev_bufs[k % nbuf], host_in[k], bytes, cudaMemcpyHostToDevice, cin))) return r;
+    return cudaEventRecord(ev_in[k], cin);
+  };
+  if ((e = copy_in(0))) return fail(e, "copy-in");
+  for (uint32_t k = 0; k < nbatch; ++k) {
+    // the next batch's copy-in is enqueued before this batch's sort: radsort_sort
+    // waits on its stream between MSD levels, so what must overlap it goes first
+    if (k + 1 < nbatch && (e = copy_in(k + 1))) return fail(e, "copy-in");
+    if ((e = cudaStreamWaitEvent(st, ev_in[k], 0))) return fail(e, "wait copy-in");
+    rs = radsort_sort(dev_bufs[k % nbuf], dev_tmp, n, rec_size, key_size, stream);
+    if (rs) {
+      const std::string d = g_detail;
+      cudaStreamSynchronize(cin);
+      cudaStreamSynchronize(cout);
+      cleanup();
+      g_detail = d;
+      return rs;
+    }
+    if ((e = cudaEventRecord(ev_sorted[k], st)) || (e = cudaStreamWaitEvent(cout, ev_sorted[k], 0)) ||
+        (e = cudaMemcpyAsync(host_out[k], dev_bufs[k % nbuf], bytes, cudaMemcpyDeviceToHost, cout)) ||
+        (e = cudaEventRecord(ev_out[k], cout)))
+      return fail(e, "copy-out");
+  }
+  if ((e = cudaStreamSynchronize(cout)) || (e = cudaStreamSynchronize(cin)) || (e = cudaStreamSynchronize(st)))
+    return fail(e, "synchronize");
+  cleanup();
+  return RADSORT_OK;
+}
+
 radsort_status radsort_locate_bucket(const uint64_t* hist256, uint64_t q, uint32_t* bucket, uint64_t* before) {
   if (!hist256 || !bucket || !before) return RADSORT_ERR_INVALID_ARG;
   uint64_t acc = 0;

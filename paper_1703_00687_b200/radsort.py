@@ -17,7 +17,7 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_NOT_INITIALIZED, ERR_CUDA, ERR_NCCL, E
 KERNEL_CLASSES = ["sample", "hist", "plan", "scatter", "children", "local", "multi", "gather"]
 
 # every symbol include/radsort.h declares
-EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
+EXPORTS = ["radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_host_stream", "radsort_sort_multi", "radsort_locate_bucket",
            "radsort_set_timing", "radsort_last_stats", "radsort_error_string", "radsort_finalize",
            "radsort_version", "radsort_loopback_create", "radsort_loopback_destroy", "radsort_sort_multi_loopback",
            "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split", "radsort_tinybench",
@@ -58,6 +58,7 @@ def _load():
     L.radsort_init.argtypes = [i32]
     L.radsort_sort.argtypes = [vp, vp, u64, u32, u32, vp]
     L.radsort_sort_host.argtypes = [vp, u64, u32, u32, vp]
+    L.radsort_sort_host_stream.argtypes = [vp, vp, u32, u64, u32, u32, vp, u32, vp, vp]
     L.radsort_sort_multi.argtypes = [vp, vp, u64, u64, ctypes.POINTER(u64), u32, u32, vp, vp]
     L.radsort_locate_bucket.argtypes = [vp, u64, ctypes.POINTER(u32), ctypes.POINTER(u64)]
     L.radsort_set_timing.argtypes = [i32]
@@ -80,8 +81,8 @@ def _load():
     L.radsort_comm_get_unique_id.argtypes = [vp]
     L.radsort_comm_init.argtypes = [vp, i32, i32, i32, ctypes.POINTER(vp)]
     L.radsort_comm_destroy.argtypes = [vp]
-    for f in ("radsort_plan_fused", "radsort_tinysort", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_multi", "radsort_locate_bucket",
-              "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
+    for f in ("radsort_plan_fused", "radsort_tinysort", "radsort_comm_get_unique_id", "radsort_comm_init", "radsort_comm_destroy", "radsort_init", "radsort_sort", "radsort_sort_host", "radsort_sort_host_stream", "radsort_sort_multi",
+              "radsort_locate_bucket", "radsort_set_timing", "radsort_last_stats", "radsort_loopback_create", "radsort_loopback_destroy",
               "radsort_sort_multi_loopback", "radsort_plan_quotas", "radsort_plan_digit", "radsort_plan_equal_split",
               "radsort_tinybench", "radsort_unique_count"):
         getattr(L, f).restype = i32
@@ -142,6 +143,22 @@ def sort_host(records, key_size: int, stream=None) -> None:
     else:
         ptr, n, R = records.data_ptr(), records.shape[0], records.shape[1]
     _check(lib.radsort_sort_host(ctypes.c_void_p(ptr), n, R, key_size, _stream_ptr(stream)))
+
+
+def sort_host_stream(host_in, host_out, key_size: int, dev_bufs, dev_tmp, stream=None) -> None:
+    """Pipelined end-to-end sort of a list of host batches (pinned uint8 tensors [n, R], all the
+    same shape): host_out[k] = sorted(host_in[k]).  dev_bufs: >= 2 device tensors of the batch's
+    size (3 overlap the sort with both copies), dev_tmp: one more.  radsort_sort_host_stream."""
+    assert len(host_in) == len(host_out) and len(host_in) > 0 and len(dev_bufs) >= 2
+    n, R = host_in[0].shape
+    for t in list(host_in) + list(host_out) + list(dev_bufs) + [dev_tmp]:
+        assert tuple(t.shape) == (n, R), "every batch and buffer must have the same [n, R] shape"
+    arr = ctypes.c_void_p * len(host_in)
+    hin = arr(*[t.data_ptr() for t in host_in])
+    hout = arr(*[t.data_ptr() for t in host_out])
+    bufs = (ctypes.c_void_p * len(dev_bufs))(*[t.data_ptr() for t in dev_bufs])
+    _check(lib.radsort_sort_host_stream(hin, hout, len(host_in), n, R, key_size, bufs, len(dev_bufs),
+                                        ctypes.c_void_p(dev_tmp.data_ptr()), _stream_ptr(stream)))
 
 
 def sort_multi(records, tmp, n_local: int, key_size: int, group=None, stream=None) -> int:

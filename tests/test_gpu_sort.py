@@ -146,6 +146,41 @@ def test_sort_host_end_to_end():
     assert oracle.compare(h.numpy(), oracle.sort(a, 16), 16) == -1
 
 
+@pytest.mark.parametrize("nbuf", [2, 3])
+@pytest.mark.parametrize("R,K,n", [(32, 16, 300_001), (8, 8, 1_000_003), (16, 8, 70_000), (24, 8, 5)])
+def test_sort_host_stream_pipelined_batches(nbuf, R, K, n):
+    # radsort_sort_host_stream: every batch a different input (distribution and seed),
+    # batch k staged in buffer k % nbuf, copies overlapped with the sorts; each
+    # output against the oracle, and the in-place form (host_out = host_in)
+    import paper_1703_00687_b200 as rs
+
+    dists = ["uniform", "zipf", "few", "sorted", "equal"]
+    ins = [dg.generate(n, R, K, dists[k], seed=100 + k) for k in range(5)]
+    h_in = [torch.from_numpy(a.copy()).pin_memory() for a in ins]
+    h_out = [torch.empty_like(h).pin_memory() for h in h_in]
+    dev = torch.device("cuda", 0)
+    bufs = [torch.full((n, R), POISON, dtype=torch.uint8, device=dev) for _ in range(nbuf)]
+    tmp = torch.empty((n, R), dtype=torch.uint8, device=dev)
+    rs.sort_host_stream(h_in, h_out, K, bufs, tmp)
+    for k, a in enumerate(ins):
+        assert oracle.compare(h_out[k].numpy(), oracle.sort(a, K), K) == -1, f"batch {k}"
+        assert np.array_equal(h_in[k].numpy(), a), "input batch modified"
+    rs.sort_host_stream(h_in[:3], h_in[:3], K, bufs, tmp)  # in place
+    for k in range(3):
+        assert oracle.compare(h_in[k].numpy(), oracle.sort(ins[k], K), K) == -1, f"in-place batch {k}"
+
+
+def test_sort_host_stream_rejects_bad_arguments():
+    import paper_1703_00687_b200 as rs
+
+    h = torch.zeros((100, 8), dtype=torch.uint8).pin_memory()
+    d = torch.zeros((100, 8), dtype=torch.uint8, device="cuda")
+    with pytest.raises(AssertionError):
+        rs.sort_host_stream([h], [h], 8, [d], d)  # one device buffer
+    with pytest.raises(rs.RadsortError):
+        rs.sort_host_stream([h], [h], 3, [d, d.clone()], d.clone())  # K = 3
+
+
 def test_device_datagen_matches_host_mirror():
     from datagen import device as dd
 
