@@ -32,7 +32,7 @@ for st in $STAGES; do
       timeout 900 ncu --set full --import-source on --clock-control none -k regex:"^$2" --launch-skip $3 -c 1 -o $O/${1}_$4 \
         python bench.py --config $1 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_${1}_$4.log 2>&1; echo "ncu $1 $4 rc=$?"
       # summarised here (the reports are too big to bring back): counters, stalls, hot lines, DRAM traffic
-      { echo "=== $1 $4 (ncu --set full --clock-control none, 1 launch; tools/r02c_final.sh)"; python tools/ncu_report.py full $O/${1}_$4.ncu-rep --lines 25; } > $O/ncu_${1}_$4.txt 2>&1
+      { echo "=== $1 $4 (ncu --set full --clock-control none, 1 launch; tools/r02d_final.sh)"; python tools/ncu_report.py full $O/${1}_$4.ncu-rep --lines 25; } > $O/ncu_${1}_$4.txt 2>&1
       rm -f $O/${1}_$4.ncu-rep
     done ;;
   esac
