@@ -589,6 +589,8 @@ struct Sorter {
     const int wide_cfg = wc ? atoi(wc) : 2;  // measured: c4 wide scatter 13.75 (1) vs 13.13 ms (2)
     const char* we = getenv("RADSORT_WIDE");
     const int wide_mode = WIDE_BUILT ? (we ? atoi(we) : 1) : 0;
+    const char* wr = getenv("RADSORT_WIDE_MIN_R");  // smallest record size the default rule applies to
+    const int wide_min_r = wr ? atoi(wr) : 24;
     int occ_w = 1;
     if constexpr (WIDE_BUILT) if (pre && wide_mode) {
       smem_attr(ctx, k_scatter<R, K, TBW, SBW, 1, true, false, 10>, TBW + SCATTER_PAD);
@@ -641,6 +643,7 @@ struct Sorter {
       }
     }
     int cur = 0;
+    bool ctl_fresh = false;  // h_ctl equals the device control block (no kernel since its read)
     const int max_levels = 2 * K + 4;
     static const char* level_names[] = {"radsort level 0", "radsort level 1", "radsort level 2", "radsort level 3",
                                         "radsort level 4", "radsort level 5", "radsort level 6", "radsort level 7",
@@ -664,7 +667,7 @@ struct Sorter {
           const double avg = (double)level_recs / n_large;
           wide = wide_mode == 3 ? avg >= 64.0
                                 : (wide_mode == 2 ? avg >= 2048.0
-                                                  : (R >= 24 && avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
+                                                  : (R >= wide_min_r && avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
         }
         if (wide) {  // the workspace is sized for 8-bit levels: grow it where a wide level needs more
           // (between levels: the previous level's histograms, bases and tile prefixes are dead)
@@ -696,8 +699,18 @@ struct Sorter {
         stats.kernel_launches[RADSORT_K_PLAN]++;
       }
       RS_CUDA(cudaGetLastError());
-      RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-      RS_CUDA(cudaStreamSynchronize(st));
+      if (ctl_fresh && !n_large && level > 0) {
+        // nothing but this k_prep ran since the last control-block read (the previous
+        // level had Large segments only): mirror k_prep's reset on the host copy
+        // instead of a D2H + host sync (one sync less per sort: c1 is sync-bound)
+        Ctl& h = *ctx->h_ctl;
+        h.tiles_total = h.scatter_ticket = h.n_large_next = 0;
+        h.rec_large_next = 0;
+        h.n_local[nxt] = h.n_local_small[nxt] = h.n_local_med[nxt] = h.max_local_len[nxt] = 0;
+      } else {
+        RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaStreamSynchronize(st));
+      }
       Ctl c = *ctx->h_ctl;
       if (level == 0) stats.first_digit = c.d0;
       const uint32_t nloc = c.n_local[cur];
@@ -733,6 +746,7 @@ struct Sorter {
       }
       tm.flush(stats);
       if (c.n_large_next == 0 && nloc == 0 && n_large == 0) break;
+      ctl_fresh = nloc == 0;  // no kernel launched since h_ctl was read
       n_large = c.n_large_next;
       level_recs = c.rec_large_next;
       cur = nxt;
