@@ -65,6 +65,7 @@ struct Ctl {
   uint32_t n_probe;                          // probe-key table entries used this sort
   uint32_t n_local_small[2];                 // Local list entries of <= small_cap<R>() records (by parity)
   uint32_t n_local_med[2];                   // ... of small_cap < len <= med_cap<R>() records
+  uint32_t dup_est;                          // k_dupest: sampled keys that met an equal earlier sample
   unsigned long long rec_large_next;          // records of the entries appended to Large[nxt] this level
   unsigned long long prof[16];  // phase cycle counters (RADSORT_PHASE_PROF builds only)
 };

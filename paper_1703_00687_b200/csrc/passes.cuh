@@ -90,6 +90,43 @@ __global__ void k_sample(Seg* large0, Ctl* ctl, const uint8_t* __restrict__ recs
   }
 }
 
+// ------------------------------------------------------------- k_dupest
+// Duplicate-key estimate for the wide-level rule of R < 24: S keys
+// at evenly spaced positions are hashed to 64 bits and inserted into an
+// open-addressing table (zeroed scratch at the head of tmp, 4 S slots); a
+// sample that meets an equal hash counts in Ctl::dup_est.  Two records share
+// a key with probability p2 ~ dup_est / (S^2 / 2), so a record has ~ p2 n
+// equal partners in the input: the 10-bit level leaves bins close to the
+// CTA-local capacity, which sort slowly when their keys repeat (kmc), so
+// R < 24 takes it only where p2 n is small.
+template <int R, int K>
+__global__ void __launch_bounds__(256) k_dupest(Ctl* ctl, const uint8_t* __restrict__ recs, uint32_t n, uint32_t S,
+                                                unsigned long long* table, uint32_t tmask) {
+  const uint32_t i = blockIdx.x * 256u + threadIdx.x;
+  if (i >= S) return;
+  const uint64_t pos = (uint64_t)i * n / S;
+  const Key<K> k = key_of<R, K>(ldg_rec<R>(recs + pos * R));
+  uint64_t h = k.w0;
+  if constexpr (K == 16) {
+    uint64_t g = k.w1 + 0x9E3779B97F4A7C15ull;
+    g = (g ^ (g >> 30)) * 0xBF58476D1CE4E5B9ull;
+    h ^= g ^ (g >> 31);
+  }
+  h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
+  h = (h ^ (h >> 27)) * 0x94D049BB133111EBull;
+  h = (h ^ (h >> 31)) | 1ull;  // never the empty slot's 0
+  uint32_t slot = (uint32_t)(h >> 32) & tmask;
+  for (int p = 0; p < 256; ++p) {
+    const unsigned long long old = atomicCAS(&table[slot], 0ull, (unsigned long long)h);
+    if (old == 0ull) return;
+    if (old == h) {
+      atomicAdd(&ctl->dup_est, 1u);
+      return;
+    }
+    slot = (slot + 1) & tmask;
+  }
+}
+
 // -------------------------------------------------------------- k_prep
 // Per level: tiles per Large segment -> exclusive prefix (single CTA), and
 // reset of the level's counters.

@@ -589,8 +589,15 @@ struct Sorter {
     const int wide_cfg = wc ? atoi(wc) : 2;  // measured: c4 wide scatter 13.75 (1) vs 13.13 ms (2)
     const char* we = getenv("RADSORT_WIDE");
     const int wide_mode = WIDE_BUILT ? (we ? atoi(we) : 1) : 0;
-    const char* wr = getenv("RADSORT_WIDE_MIN_R");  // smallest record size the default rule applies to
+    // The default rule applies to R >= 24, and to R < 24 where the sampled keys hardly repeat
+    // (k_dupest; measured: (16,8) 1 G uniform 45.6 -> 27.2 ms, (8,8) 2 G 54.0 -> 35.6, but kmc
+    // 27.7 -> 55.5 with ~100 copies per key).  RADSORT_WIDE_MIN_R=r: R >= r, no estimate.
+    const char* wr = getenv("RADSORT_WIDE_MIN_R");
     const int wide_min_r = wr ? atoi(wr) : 24;
+    constexpr uint32_t DUP_S = 1u << 18, DUP_SLOTS = 4 * DUP_S;
+    const bool dup_run = !init && !wr && R < 24 && pre && wide_mode == 1 && (double)n > 256.0 * C &&
+                         (size_t)n * R >= (size_t)DUP_SLOTS * 8 && ((uintptr_t)tmp & 7u) == 0;
+    bool wide_small_ok = false;
     int occ_w = 1;
     if constexpr (WIDE_BUILT) if (pre && wide_mode) {
       smem_attr(ctx, k_scatter<R, K, TBW, SBW, 1, true, false, 10>, TBW + SCATTER_PAD);
@@ -636,6 +643,11 @@ struct Sorter {
       if (n_large) {  // k_sample also writes the control block and the level-0 segment (k_init's Large case)
         tm.begin(RADSORT_K_SAMPLE);
         k_sample<R, K><<<1, 256, 0, st>>>(L[0], ctl, recs, n);
+        if (dup_run) {  // after k_sample (it resets the control block); tmp is free until the level-0 scatter
+          RS_CUDA(cudaMemsetAsync(tmp, 0, (size_t)DUP_SLOTS * 8, st));
+          k_dupest<R, K><<<DUP_S / 256, 256, 0, st>>>(ctl, recs, n, DUP_S, (unsigned long long*)tmp, DUP_SLOTS - 1);
+          stats.kernel_launches[RADSORT_K_SAMPLE]++;
+        }
         tm.end();
         stats.kernel_launches[RADSORT_K_SAMPLE]++;
       } else {
@@ -667,7 +679,7 @@ struct Sorter {
           const double avg = (double)level_recs / n_large;
           wide = wide_mode == 3 ? avg >= 64.0
                                 : (wide_mode == 2 ? avg >= 2048.0
-                                                  : (R >= wide_min_r && avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
+                                                  : ((R >= wide_min_r || wide_small_ok) && avg > 256.0 * C && avg <= 0.95 * 1024.0 * C));
         }
         if (wide) {  // the workspace is sized for 8-bit levels: grow it where a wide level needs more
           // (between levels: the previous level's histograms, bases and tile prefixes are dead)
@@ -713,6 +725,12 @@ struct Sorter {
       }
       Ctl c = *ctx->h_ctl;
       if (level == 0) stats.first_digit = c.d0;
+      if (level == 0 && dup_run) {  // p2 n < 1/4 (at least 4 hits: the estimate's noise floor)
+        const double thr = std::max(4.0, (double)DUP_S * DUP_S / (8.0 * n));
+        wide_small_ok = (double)c.dup_est <= thr;
+        if (log) fprintf(stderr, "[radsort] duplicate estimate: %u of %u sampled keys repeat (threshold %.0f): wide levels %s\n",
+                         c.dup_est, DUP_S, thr, wide_small_ok ? "on" : "off");
+      }
       const uint32_t nloc = c.n_local[cur];
       if (log)
         fprintf(stderr, "[radsort] level %d%s: large=%u tiles=%u -> large_next=%u local=%u (max %u)\n", level,

@@ -49,3 +49,30 @@ def test_full_config(cfg, samples):
     st = rs.last_stats()
     if cfg == "c2":
         assert st["first_digit"] == 3  # digits 0..2 constant
+
+
+@pytest.mark.parametrize("R,K,n,dist,wide", [(16, 8, 1_000_000_000, "uniform", 1), (16, 16, 413_000_000, "kmer", 0)])
+def test_full_wide_rule_small_records(R, K, n, dist, wide):
+    """The sizes where the wide-level rule fires for R < 24 (8-bit level-1 children above the
+    CTA-local capacity): taken for distinct keys, not for the duplicate-heavy k-mer stream."""
+    import paper_1703_00687_b200 as rs
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 2.2 * n * R:
+        pytest.skip(f"needs {2.2 * n * R / 1e9:.0f} GB of device memory")
+    rs.init(0)
+    rec = dd.generate_tensor(n, R, K, dist, "random", 20261021)
+    dig_in = verify.digest(rec.data_ptr(), n, R)
+    host_in = rec.cpu().numpy()
+    tmp = torch.empty_like(rec)
+    rs.sort(rec, tmp, K)
+    torch.cuda.synchronize()
+    del tmp
+    bad, first = verify.sorted_check(rec.data_ptr(), n, R, K)
+    assert bad == 0, f"{bad} adjacent inversions, first at {first}"
+    assert verify.digest(rec.data_ptr(), n, R) == dig_in, "output is not a permutation of the input"
+    rng = np.random.default_rng(20261021)
+    for i in sorted(set([0, n - 1] + [int(x) for x in rng.integers(0, n, 3)])):
+        lt, le = oracle.rank_bounds(host_in, K, rec[i].cpu().numpy())
+        assert lt <= i < le, f"output position {i} holds a key of rank [{lt}, {le})"
+    assert rs.last_stats()["wide_levels"] == wide

@@ -532,3 +532,24 @@ def test_wide_level_default_rule(R, K, monkeypatch):
     monkeypatch.setenv("RADSORT_WIDE", "0")
     check(dg.generate(n, R, K, "uniform", seed=7), K)
     assert _wide_levels() == 0
+
+
+@pytest.mark.parametrize("R,K", [(16, 8), (16, 16), (8, 8)])
+def test_wide_level_small_records_need_distinct_keys(R, K, monkeypatch):
+    # R < 24 takes the default rule's wide level only where the sampled keys hardly repeat
+    # (k_dupest).  Two level-0 bins (the leading key byte takes two values) of
+    # (256 C, 0.95 * 1024 C] records each: level 1 is wide for distinct keys, 8-bit for repeated ones
+    monkeypatch.delenv("RADSORT_WIDE", raising=False)
+    monkeypatch.delenv("RADSORT_WIDE_MIN_R", raising=False)
+    n = int(2 * 300 * C_of(R)) + 11
+    a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=31)
+    a[:, K - 1] &= 1
+    check(a, K)
+    assert _wide_levels() == 1
+    b = a.copy()
+    b[:, :K] = a[np.arange(n) % 50_021, :K]  # ~50 K distinct keys, ~100 copies each
+    check(b, K)
+    assert _wide_levels() == 0
+    monkeypatch.setenv("RADSORT_WIDE_MIN_R", "8")  # the rule without the estimate
+    check(b, K)
+    assert _wide_levels() == 1
