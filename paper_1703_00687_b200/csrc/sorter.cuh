@@ -598,6 +598,8 @@ struct Sorter {
     const bool dup_run = !init && !wr && R < 24 && pre && wide_mode == 1 && (double)n > 256.0 * C &&
                          (size_t)n * R >= (size_t)DUP_SLOTS * 8 && ((uintptr_t)tmp & 7u) == 0;
     bool wide_small_ok = false;
+    // p2 n < 1/4 (at least 4 hits: the estimate's noise floor)
+    auto dup_few = [n](uint32_t hits) { return (double)hits <= std::max(4.0, (double)DUP_S * DUP_S / (8.0 * n)); };
     int occ_w = 1;
     if constexpr (WIDE_BUILT) if (pre && wide_mode) {
       smem_attr(ctx, k_scatter<R, K, TBW, SBW, 1, true, false, 10>, TBW + SCATTER_PAD);
@@ -649,6 +651,13 @@ struct Sorter {
           stats.kernel_launches[RADSORT_K_SAMPLE]++;
         }
         tm.end();
+        if (dup_run && (double)n <= 0.95 * 1024.0 * C) {
+          // level 0 itself is in the rule's window (one 10-bit pass + the local sort instead of
+          // two 8-bit passes): the estimate is needed now, at the price of one more host sync
+          RS_CUDA(cudaMemcpyAsync(ctx->h_ctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+          RS_CUDA(cudaStreamSynchronize(st));
+          wide_small_ok = dup_few(ctx->h_ctl->dup_est);
+        }
         stats.kernel_launches[RADSORT_K_SAMPLE]++;
       } else {
         k_init<<<1, 1, 0, st>>>(L[0], Lo[0], ctl, n, C);
@@ -725,11 +734,10 @@ struct Sorter {
       }
       Ctl c = *ctx->h_ctl;
       if (level == 0) stats.first_digit = c.d0;
-      if (level == 0 && dup_run) {  // p2 n < 1/4 (at least 4 hits: the estimate's noise floor)
-        const double thr = std::max(4.0, (double)DUP_S * DUP_S / (8.0 * n));
-        wide_small_ok = (double)c.dup_est <= thr;
-        if (log) fprintf(stderr, "[radsort] duplicate estimate: %u of %u sampled keys repeat (threshold %.0f): wide levels %s\n",
-                         c.dup_est, DUP_S, thr, wide_small_ok ? "on" : "off");
+      if (level == 0 && dup_run) {
+        wide_small_ok = dup_few(c.dup_est);
+        if (log) fprintf(stderr, "[radsort] duplicate estimate: %u of %u sampled keys repeat: wide levels %s\n",
+                         c.dup_est, DUP_S, wide_small_ok ? "on" : "off");
       }
       const uint32_t nloc = c.n_local[cur];
       if (log)

@@ -534,14 +534,16 @@ def test_wide_level_default_rule(R, K, monkeypatch):
     assert _wide_levels() == 0
 
 
-@pytest.mark.parametrize("R,K", [(16, 8), (16, 16), (8, 8)])
-def test_wide_level_small_records_need_distinct_keys(R, K, monkeypatch):
+@pytest.mark.parametrize("R,K,bins", [(16, 8, 300), (16, 16, 300), (8, 8, 300), (16, 8, 600)])
+def test_wide_level_small_records_need_distinct_keys(R, K, bins, monkeypatch):
     # R < 24 takes the default rule's wide level only where the sampled keys hardly repeat
-    # (k_dupest).  Two level-0 bins (the leading key byte takes two values) of
-    # (256 C, 0.95 * 1024 C] records each: level 1 is wide for distinct keys, 8-bit for repeated ones
+    # (k_dupest).  The rule's window is (256 C, 0.95 * 1024 C] records per segment:
+    # with 600 C records the whole input is in it (level 0 is wide, decided before the pass);
+    # with 1200 C only the two level-0 bins are (the leading key byte takes two values: level 1
+    # is wide).  Repeated keys: no wide level
     monkeypatch.delenv("RADSORT_WIDE", raising=False)
     monkeypatch.delenv("RADSORT_WIDE_MIN_R", raising=False)
-    n = int(2 * 300 * C_of(R)) + 11
+    n = int(2 * bins * C_of(R)) + 11
     a = dg.generate(n, R, K, "uniform", payload="index" if R > K else "random", seed=31)
     a[:, K - 1] &= 1
     check(a, K)
