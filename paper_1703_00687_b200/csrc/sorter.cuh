@@ -586,7 +586,9 @@ struct Sorter {
     constexpr int TBW2 = 2 * TB, SBW2 = 512;  // (default) two 512-thread CTAs per SM, two digits per thread
     constexpr uint32_t TW = tile_recs<R, TBW, SBW>(), TW2 = tile_recs<R, TBW2, SBW2>();
     const char* wc = getenv("RADSORT_WIDE_CFG");
-    const int wide_cfg = wc ? atoi(wc) : 2;  // measured: c4 wide scatter 13.75 (1) vs 13.13 ms (2)
+    // measured: c4 (R = 32) wide scatter 13.75 (1) vs 13.13 ms (2); (16,8) 1 G 25.8 (1) vs 27.4 ms per sort (2: that
+    // instance spills at its 64 registers), (16,16) 26.7 vs 28.4, (8,8) 2 G 36.0 vs 36.3
+    const int wide_cfg = wc ? atoi(wc) : (R < 24 ? 1 : 2);
     const char* we = getenv("RADSORT_WIDE");
     const int wide_mode = WIDE_BUILT ? (we ? atoi(we) : 1) : 0;
     // The default rule applies to R >= 24, and to R < 24 where the sampled keys hardly repeat

@@ -555,3 +555,15 @@ def test_wide_level_small_records_need_distinct_keys(R, K, bins, monkeypatch):
     monkeypatch.setenv("RADSORT_WIDE_MIN_R", "8")  # the rule without the estimate
     check(b, K)
     assert _wide_levels() == 1
+
+
+@pytest.mark.parametrize("R,K", [(8, 8), (16, 8), (32, 16), (40, 16)])
+@pytest.mark.parametrize("cfg", ["1", "2"])
+def test_wide_level_both_tile_shapes(R, K, cfg, monkeypatch):
+    # RADSORT_WIDE_CFG: the wide pass as one 1024-thread CTA per SM (1, default for R < 24) or two
+    # 512-thread CTAs (2, default for R >= 24): both shapes on both record-size classes
+    monkeypatch.setenv("RADSORT_WIDE", "2")
+    monkeypatch.setenv("RADSORT_WIDE_CFG", cfg)
+    for n, dist in ((1_200_011, "uniform"), (300_007, "zipf")):
+        check(dg.generate(n, R, K, dist, payload="index" if R > K else "random", seed=515 + n), K)
+        assert _wide_levels() >= 1
